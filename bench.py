@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark of the LongFlow fused decode step (BASELINE.json metric) -- one JSON line on rank 0.
+
+  python bench.py [--gpus N --steps K --warmup W --workload r --scaling weak|strong]
+  python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+         --master-port P bench.py --gpus N ...
+  python bench.py --impl reference ...      # the fp64 CPU oracle on the host cores
+
+A "step" is one lf_decode_step over every (sequence, kv head) unit of the rank's shard: the whole
+hot path (logits, softmax, PV, LongFlowScore, argmin, in-place eviction) on a FULL static cache,
+so every step evicts.  value = tokens/s summed over ranks (one token per sequence per step).
+Inputs of 8 pre-generated steps live in HBM; the cache (8.6 GB per GPU for `r`) is far larger
+than L2, so no L2 flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from lf_synth import CONFIGS, Synth, Workload, bits, random_cache, sweep_workload  # noqa: E402
+
+METRIC = "fused decode-step tokens/s (LongFlow attention+score+evict, full static cache)"
+
+
+def workload_of(tag: str) -> Workload:
+    if tag.startswith("sweep"):
+        _, b, n = tag.split("_")
+        return sweep_workload(int(b[1:]), int(n[1:]))
+    return CONFIGS[tag]
+
+
+def alg_bytes_per_step(wl: Workload, B: int, out_bytes: int) -> int:
+    """SURVEY.md 8(d) D.3 per unit: 4Nd (K+V read) + 4d (k*,v* read) + 4d (victim write)
+    + 2Gd (q) + G d out_bytes (out) + 4 (slot)."""
+    d, N, G = wl.d, wl.N, wl.G
+    per_unit = 4 * N * d + 4 * d + 4 * d + 2 * G * d + G * d * out_bytes + 4
+    return per_unit * B * wl.Hkv
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profiles(tag: str):
+    """dram bytes read+write per launch from the committed `ncu --set full` summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(tag)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    def __init__(self, device_index: int, period=0.02):
+        self.period = period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg / --impl reference): the fp64 oracle as it stands, on host cores
+# ------------------------------------------------------------------------------------------------
+
+def oracle_rate(wl: Workload, B_total: int, seconds: float = 12.0, seed: int = 0):
+    """Times the oracle's same-step decode on a bounded sample of the workload (full caches of
+    a few sequences, all kv heads), extrapolated linearly in units to the full batch (the cost
+    is exactly linear in units).  Returns (tokens/s, cores, sample description, s/step)."""
+    import oracle
+    cores = os.cpu_count() or 1
+
+    def run(Bs, steps):
+        orc = oracle.OracleCache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, nthreads=cores)
+        k, v = random_cache(Bs, wl.Hkv, wl.N, wl.d, seed=seed)
+        orc.K[...] = bits(k)
+        orc.V[...] = bits(v)
+        orc.n_valid[...] = wl.N
+        syn = Synth(Workload(wl.tag, Bs, wl.Hq, wl.Hkv, wl.d, wl.N, 0, steps), seed=seed)
+        ins = [tuple(bits(x) for x in syn.step()) for _ in range(steps)]
+        t0 = time.perf_counter()
+        for q, kn, vn in ins:
+            orc.step(q, kn, vn)
+        return time.perf_counter() - t0
+
+    t1 = run(1, 1)
+    units_per_s = wl.Hkv / max(t1, 1e-9)
+    Bs = max(1, min(B_total, int(units_per_s * seconds / wl.Hkv / 2)))
+    steps = 2
+    t = run(Bs, steps)
+    sec_per_unit_step = t / (Bs * wl.Hkv * steps)
+    sec_per_step = sec_per_unit_step * B_total * wl.Hkv
+    desc = (f"{Bs} sequences x {wl.Hkv} kv heads x {steps} steps of workload '{wl.tag}' "
+            f"(full cache N={wl.N}), {t:.1f} s on {cores} threads, extrapolated linearly to batch {B_total}")
+    return B_total / sec_per_step, cores, desc, sec_per_step
+
+
+def run_reference(args, wl, B_total):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    vals = []
+    descs = None
+    for _ in range(max(args.warmup, 0)):
+        pass   # the oracle has no warm-up state; each timed step is a fresh bounded sample
+    for _ in range(args.steps):
+        v, cores, desc, sps = oracle_rate(wl, B_total, seconds=args.ref_seconds)
+        vals.append(v)
+        descs = (cores, desc, sps)
+    value = float(np.median(vals))
+    cores, desc, sps = descs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sps * 1e3, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_of(args, wl, B_total, None),
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, wl, B_total, plan):
+    c = {"workload": wl.tag, "global_batch": B_total, "batch_per_gpu": B_total // max(args.gpus, 1),
+         "num_q_heads": wl.Hq, "num_kv_heads": wl.Hkv, "head_dim": wl.d, "budget": wl.N,
+         "cache": "full (every step evicts)", "out_dtype": args.out_dtype,
+         "parallelism": f"dp{args.gpus} by sequence (no collective on the hot path)",
+         "l2": "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(
+             2 * wl.N * wl.d * 2 * wl.Hkv * B_total / max(args.gpus, 1) / 1e9)}
+    if plan:
+        c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"]})
+    return c
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="r", help="tiny | q7 | q3 | r | f1 | sweep_b<B>_n<N>")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU holds the workload's batch; strong: the batch is split")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--split-tokens", type=int, default=0)
+    ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--no-graph", action="store_true", help="launch steps directly instead of a CUDA graph")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--seed", type=int, default=0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus and ws > 1:
+        print(f"warning: WORLD_SIZE={ws} != --gpus {args.gpus}", file=sys.stderr)
+    args.gpus = max(ws, 1) if ws > 1 else args.gpus
+    wl = workload_of(args.workload)
+    B_total = wl.B * args.gpus if args.scaling == "weak" else wl.B
+    if args.impl == "reference":
+        return run_reference(args, wl, B_total)
+    if args.gpus > 1 and ws == 1:
+        print("--gpus > 1 needs torchrun (one process per GPU)", file=sys.stderr)
+        return 2
+
+    from paper_2603_11504_b200 import Cache
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    if B_total % args.gpus:
+        raise SystemExit("global batch not divisible by the GPU count")
+    B = B_total // args.gpus
+    b0 = rank * B
+
+    cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
+                  split_tokens=args.split_tokens, device=local)
+    plan = cache.plan()
+    K, V, nv = cache.views()
+    k0, v0 = random_cache(B, wl.Hkv, wl.N, wl.d, seed=args.seed, device=dev, b0=b0)
+    K.copy_(k0)
+    V.copy_(v0)
+    nv.fill_(wl.N)
+    del k0, v0
+    syn = Synth(wl, seed=args.seed, device=dev, B=B, b0=b0)
+    pool = [syn.step() for _ in range(8)]
+    out, slot, _ = cache.new_outputs()
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize(dev)
+
+    def step(i):
+        q, kn, vn = pool[i % len(pool)]
+        cache.decode_step(q, kn, vn, out, slot, stream=stream)
+
+    # warm-up (W steps), then optionally capture a graph of the K timed steps (launch-bound configs)
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize(dev)
+    graph = None
+    if not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(args.steps):
+                step(i)
+        torch.cuda.synchronize(dev)
+        graph.replay()     # one untimed replay (graph upload)
+        torch.cuda.synchronize(dev)
+
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        if graph is not None:
+            with torch.cuda.stream(stream):
+                graph.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    if pg:
+        pg.barrier()
+    ms = ev0.elapsed_time(ev1)
+    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if pg:
+        pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
+        # statistics gather (off the hot path): per-rank slot checksums
+        chk = torch.tensor([float(slot.double().sum())], device=dev, dtype=torch.float64)
+        allchk = [torch.zeros_like(chk) for _ in range(ws)]
+        pg.all_gather(allchk, chk)
+    ms_max = float(ms_t.item())
+    ms_step = ms_max / args.steps
+    value = B_total / (ms_step / 1e3)
+
+    # ---- end to end through the public host API: H2D of the step's inputs + D2H of out/slot
+    e2e = None
+    q0, kn0, vn0 = pool[0]
+    hq = [t.cpu().pin_memory() for t in pool[0]]
+    oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    sh = torch.empty(slot.shape, dtype=torch.int32).pin_memory()
+    e2e_steps = max(10, min(args.steps, 100))
+    for _ in range(3):
+        cache.decode_step_host(*hq, oh, sh, stream=stream)
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        cache.decode_step_host(*hq, oh, sh, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev, dtype=torch.float64)
+    if pg:
+        pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
+    h2d = sum(t.numel() * t.element_size() for t in hq)
+    d2h = oh.numel() * oh.element_size() + sh.numel() * 4
+    e2e = {"value": B_total / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": h2d * args.gpus, "d2h_bytes_per_step": d2h * args.gpus,
+           "ms_per_step": float(e_ms.item()), "steps": e2e_steps, "api": "lf_decode_step_host"}
+
+    out_bytes = 2 if args.out_dtype == "bf16" else 4
+    alg = alg_bytes_per_step(wl, B, out_bytes)
+    peak, peak_src = peaks()
+    achieved = alg / (ms_step / 1e3) / 1e9
+    traffic = traffic_from_profiles(f"{wl.tag}_B{B}_{plan['kernel']}")
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "latency_us": ms_step * 1e3,
+        "steps_per_s": 1e3 / ms_step, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded bf16 N(0,1) K/V, query random walk)",
+        "config": config_of(args, wl, B_total, plan),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": f"lf decode ({plan['kernel']})",
+                     "alg_bytes_per_launch": alg},
+        "hbm_gbs_aggregate": achieved * args.gpus,
+        "e2e": e2e,
+        "gpu_launches": args.steps * cache.kernels_per_step(),
+        "clocks": clk.summary(),
+        "graph": graph is not None,
+    }
+    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
+        v, cores, desc, sps = oracle_rate(wl, B_total, seconds=args.ref_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,136 @@
+/*
+ * longflow.h -- C ABI of the B200-native LongFlow fused decode-step operator.
+ *
+ * Citation key: P:n = PAPER.md line n (arXiv 2603.11504), S:n = SPEC.md line n; readings
+ * R1..R17 are listed in DESIGN.md ("Readings of the paper").
+ *
+ * The operation (Alg. 1; Eq. 1, Eq. 5, Eq. 6): for every unit
+ * u = (sequence b, kv head h) of a static, pre-allocated KV cache one decode step
+ *   - attends the G = Hq/Hkv query heads hq = h*G + g of the current token over the n valid
+ *     cached tokens plus the current token (R1),
+ *   - scores every cached token with LongFlowScore I_j = (1/G) sum_g alpha_gj ||v_j||_1
+ *     (Eq. 6, mean over the query group R2) from the same pass,
+ *   - selects slot = lowest-index argmin_j I_j (R7) and overwrites it in place
+ *     with the current token's K/V (Fig. 2) -- or, while n < budget, appends
+ *     the token at slot n (R11).
+ *
+ * Conventions (all entry points):
+ *   - Tensor arguments are DEVICE pointers unless the name ends in _host.  bf16 means IEEE
+ *     bfloat16 bit patterns (uint16).  Row-major layouts are given per argument.
+ *   - The caller owns every tensor it passes.  The cache slab is library-owned (one
+ *     cudaMalloc in lf_cache_create) or caller-owned (device_buf != NULL); lf_cache_destroy
+ *     frees only library-owned memory.  A handle must outlive all work enqueued with it.
+ *   - Errors are status codes; no exception or abort crosses the ABI.  Arguments are
+ *     validated on the host before any launch; launch failures map to LF_ERR_CUDA with the
+ *     CUDA error text in lf_last_error().  Asynchronous device faults surface at the
+ *     caller's next synchronisation.
+ *   - Device entry points only enqueue work on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and never synchronise the host, so they are CUDA-graph capturable.
+ *   - A handle is not thread-safe; distinct handles (e.g. one per GPU rank) are independent
+ *     (S:169).  RoPE, if any, is applied by the caller before q/k reach the ABI.
+ */
+#ifndef LONGFLOW_H
+#define LONGFLOW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lf_cache lf_cache; /* opaque: host struct + device slab */
+
+typedef enum {
+    LF_OK = 0,
+    LF_ERR_INVALID_ARGUMENT = 1,        /* bad shape / pointer / index */
+    LF_ERR_UNSUPPORTED = 2,             /* valid but not built for (e.g. head_dim not in {64,128}) */
+    LF_ERR_OUT_OF_MEMORY = 3,
+    LF_ERR_PREFILL_EXCEEDS_BUDGET = 4,  /* "prefill exceeds budget; compress first" */
+    LF_ERR_CUDA = 5
+} lf_status;
+
+typedef enum { LF_DTYPE_BF16 = 0, LF_DTYPE_F32 = 1 } lf_dtype;
+
+typedef enum {
+    LF_EVICT_SAME_STEP = 0  /* R1: the current token is attended, then covers the victim this step */
+} lf_evict_mode;
+
+typedef enum {
+    LF_KERNEL_AUTO = 0,     /* tcgen05 path when G >= 4 and built, else the CUDA-core path */
+    LF_KERNEL_SIMT = 1,     /* CUDA-core split-KV kernel (any G <= 16) */
+    LF_KERNEL_TCGEN05 = 2   /* TMA + tcgen05 (TMEM) split-KV kernel, 2 <= G <= 8 */
+} lf_kernel;
+
+typedef struct {
+    int32_t batch;         /* sequences held by this cache (a GPU rank's shard), >= 1          */
+    int32_t num_q_heads;   /* Hq, multiple of num_kv_heads                                      */
+    int32_t num_kv_heads;  /* Hkv; query head hq reads kv head hq / (Hq/Hkv) (R2)               */
+    int32_t head_dim;      /* d in {64, 128}; other values -> LF_ERR_UNSUPPORTED                */
+    int32_t budget;        /* N >= 2 static slots per (sequence, kv head)               */
+    int32_t out_dtype;     /* lf_dtype of `out`: BF16 (production) or F32 (parity, R12)         */
+    float softmax_scale;   /* <= 0 -> 1/sqrt(head_dim) (Eq. 1, Alg. 1, R4)          */
+    int32_t mode;          /* lf_evict_mode                                                     */
+    int32_t kernel;        /* lf_kernel                                                         */
+    int32_t split_tokens;  /* tokens per split-KV CTA (multiple of 128), 0 = automatic plan     */
+} lf_cache_config;
+
+/* Bytes of the device slab for `cfg` (K, V, per-unit valid counts, staging for the host
+ * entry point), for callers that provide their own memory. */
+lf_status lf_cache_bytes(const lf_cache_config* cfg, size_t* bytes);
+
+/* Creates a cache on CUDA device `device`: every slot invalid (n_valid = 0).  device_buf ==
+ * NULL -> the library performs exactly one cudaMalloc; else device_buf (>= 256-byte
+ * aligned, buf_bytes >= lf_cache_bytes) is used and stays caller-owned.  Synchronous. */
+lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_buf,
+                          size_t buf_bytes, lf_cache** out);
+
+/* Frees library-owned memory and the handle (after synchronising its device). */
+lf_status lf_cache_destroy(lf_cache* c);
+
+/* Prefill: slots [0, n) of every kv head of sequence `seq` <- rows of
+ * k, v (bf16 [Hkv][n][d], device), n_valid[seq][*] = n; slots >= n become invalid.
+ * n > budget -> LF_ERR_PREFILL_EXCEEDS_BUDGET (SnapKV compression happens upstream).
+ * n == 0 resets the sequence.  Enqueued on `stream`. */
+lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v, int32_t n,
+                          void* stream);
+
+/* One fused decode step over the whole cache (Alg. 1 + Fig. 2 left, same-step mode R1):
+ *   q      bf16 [B][Hq][d]       current token's queries (post-RoPE)
+ *   k_new  bf16 [B][Hkv][d]      current token's key   (post-RoPE)
+ *   v_new  bf16 [B][Hkv][d]      current token's value
+ *   out    out_dtype [B][Hq][d]  attention output o_t (Eq. 1 over n cached + current token)
+ *   slot   int32 [B][Hkv]        slot now holding the current token: the evicted victim when
+ *                                the unit was full, else the append slot n
+ *   scores fp32 [B][Hkv][budget] or NULL: I_j of the pre-write cache, +INF for j >= n
+ * The victim's K/V rows are overwritten in place; n_valid grows by one for appending units.
+ * Enqueued on `stream`; no host synchronisation. */
+lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new,
+                         void* out, int32_t* slot, float* scores, void* stream);
+
+/* Same step with HOST buffers (the end-to-end entry point): copies q/k_new/v_new host ->
+ * device (pinned host memory recommended), runs lf_decode_step on `stream`, copies out and
+ * slot device -> host and synchronises `stream` before returning. Layouts as above. */
+lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new_host,
+                              const void* v_new_host, void* out_host, int32_t* slot_host,
+                              void* stream);
+
+/* Device views for snapshots and tests: K, V bf16 [B][Hkv][budget][d]; n_valid int32
+ * [B][Hkv] (one count per unit; all heads of a sequence carry the same value). */
+lf_status lf_cache_views(const lf_cache* c, void** k, void** v, int32_t** n_valid);
+
+/* The split plan the next lf_decode_step will launch: kernel id (lf_kernel), splits per
+ * unit (CTAs per cluster) and tokens per split. */
+lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
+                        int32_t* split_tokens);
+
+/* Number of CUDA kernels lf_decode_step launches per call (for launch accounting). */
+int32_t lf_kernels_per_step(const lf_cache* c);
+
+const char* lf_status_string(lf_status s);
+const char* lf_last_error(void); /* thread-local detail text of the last failure */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LONGFLOW_H */

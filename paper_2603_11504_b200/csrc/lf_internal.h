@@ -1,0 +1,45 @@
+// Internal declarations shared by the host runtime and the decode kernels (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/longflow.h"
+
+namespace lf {
+
+// Everything one decode-step launch needs (passed by value as a kernel parameter).
+struct StepParams {
+    const uint16_t* q;      // bf16 [B][Hq][d]
+    const uint16_t* k_new;  // bf16 [B][Hkv][d]
+    const uint16_t* v_new;  // bf16 [B][Hkv][d]
+    uint16_t* K;            // bf16 [B][Hkv][N][d]   (cache, updated in place)
+    uint16_t* V;            // bf16 [B][Hkv][N][d]
+    int32_t* n_valid;       // int32 [B][Hkv]
+    void* out;              // bf16 or fp32 [B][Hq][d]
+    int32_t* slot;          // int32 [B][Hkv]
+    float* scores;          // fp32 [B][Hkv][N] or nullptr
+    int32_t B, Hq, Hkv, G, d, N;
+    int32_t out_f32;        // 1: fp32 out, 0: bf16 out
+    float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip
+    int32_t splits;         // CTAs per unit (= cluster size)
+    int32_t chunk;          // tokens per CTA (multiple of 128)
+};
+
+struct Plan {
+    int32_t kernel;   // lf_kernel (resolved: SIMT or TCGEN05)
+    int32_t splits;
+    int32_t chunk;
+    int32_t smem;     // dynamic shared memory bytes per CTA
+};
+
+// CUDA-core split-KV kernel (lf_decode_simt.cu)
+bool simt_supported(int G, int d);
+Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms);
+cudaError_t simt_launch(const StepParams& p, const Plan& plan, cudaStream_t stream);
+
+// TMA + tcgen05 split-KV kernel (lf_decode_tc.cu)
+bool tc_supported(int G, int d);
+Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms);
+cudaError_t tc_launch(const StepParams& p, const Plan& plan, cudaStream_t stream);
+
+}  // namespace lf

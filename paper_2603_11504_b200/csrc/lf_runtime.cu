@@ -1,0 +1,349 @@
+// Host runtime of the LongFlow C ABI (include/longflow.h): validation, the static cache slab,
+// prefill, split planning and decode-step dispatch.  No torch types anywhere.
+//
+// Static memory ("allocations == 1"): one slab per cache holding
+//   K, V       bf16 [B][Hkv][N][d]
+//   n_valid    int32 [B][Hkv]
+//   staging    q/k_new/v_new/out/slot device copies for lf_decode_step_host
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "lf_internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+
+lf_status fail(lf_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+lf_status fail(lf_status s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+lf_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(LF_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    size_t k_off, v_off, nv_off, sq_off, sk_off, sv_off, so_off, ss_off, total;
+};
+
+Layout layout_of(const lf_cache_config& c) {
+    Layout L;
+    size_t kv = (size_t)c.batch * c.num_kv_heads * c.budget * c.head_dim * 2;
+    size_t off = 0;
+    L.k_off = off; off = align_up(off + kv, 256);
+    L.v_off = off; off = align_up(off + kv, 256);
+    L.nv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
+    L.sq_off = off; off = align_up(off + (size_t)c.batch * c.num_q_heads * c.head_dim * 2, 256);
+    L.sk_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
+    L.sv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
+    L.so_off = off; off = align_up(off + (size_t)c.batch * c.num_q_heads * c.head_dim * 4, 256);
+    L.ss_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
+    L.total = off;
+    return L;
+}
+
+lf_status validate(const lf_cache_config* c) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cfg is NULL");
+    if (c->batch < 1) return fail(LF_ERR_INVALID_ARGUMENT, "batch must be >= 1 (got %d)", c->batch);
+    if (c->num_kv_heads < 1 || c->num_q_heads < 1)
+        return fail(LF_ERR_INVALID_ARGUMENT, "head counts must be >= 1");
+    if (c->num_q_heads % c->num_kv_heads)
+        return fail(LF_ERR_INVALID_ARGUMENT, "num_q_heads %% num_kv_heads != 0 (%d, %d)",
+                    c->num_q_heads, c->num_kv_heads);
+    if (c->head_dim < 1) return fail(LF_ERR_INVALID_ARGUMENT, "head_dim must be >= 1");
+    if (c->budget < 2) return fail(LF_ERR_INVALID_ARGUMENT, "budget must be >= 2 (S:123)");
+    if (c->out_dtype != LF_DTYPE_BF16 && c->out_dtype != LF_DTYPE_F32)
+        return fail(LF_ERR_INVALID_ARGUMENT, "unknown out_dtype %d", c->out_dtype);
+    if (c->mode != LF_EVICT_SAME_STEP) return fail(LF_ERR_UNSUPPORTED, "only same-step mode is built");
+    if (c->kernel < LF_KERNEL_AUTO || c->kernel > LF_KERNEL_TCGEN05)
+        return fail(LF_ERR_INVALID_ARGUMENT, "unknown kernel %d", c->kernel);
+    if (c->split_tokens < 0 || c->split_tokens % 128)
+        return fail(LF_ERR_INVALID_ARGUMENT, "split_tokens must be a multiple of 128 (got %d)",
+                    c->split_tokens);
+    if (c->head_dim != 64 && c->head_dim != 128)
+        return fail(LF_ERR_UNSUPPORTED, "head_dim %d not built (64, 128)", c->head_dim);
+    int G = c->num_q_heads / c->num_kv_heads;
+    if (G > 16) return fail(LF_ERR_UNSUPPORTED, "group size %d > 16 not built", G);
+    if ((long long)c->batch * c->num_kv_heads > 0x7fffffff / 2)
+        return fail(LF_ERR_INVALID_ARGUMENT, "too many units");
+    if (c->budget > 65536) return fail(LF_ERR_UNSUPPORTED, "budget %d > 65536 not built", c->budget);
+    return LF_OK;
+}
+
+__global__ void fill_i32(int32_t* p, int32_t v, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = v;
+}
+
+}  // namespace
+
+struct lf_cache {
+    lf_cache_config cfg;
+    int device;
+    int num_sms;
+    void* slab;
+    size_t slab_bytes;
+    bool owns;
+    Layout L;
+    lf::Plan plan;
+};
+
+namespace {
+
+lf_status make_plan(lf_cache* c) {
+    const lf_cache_config& g = c->cfg;
+    int G = g.num_q_heads / g.num_kv_heads;
+    int units = g.batch * g.num_kv_heads;
+    bool want_tc = g.kernel == LF_KERNEL_TCGEN05 ||
+                   (g.kernel == LF_KERNEL_AUTO && G >= 4 && lf::tc_supported(G, g.head_dim));
+    if (want_tc) {
+        if (!lf::tc_supported(G, g.head_dim))
+            return fail(LF_ERR_UNSUPPORTED, "tcgen05 kernel not built for G=%d d=%d", G, g.head_dim);
+        c->plan = lf::tc_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+    } else {
+        if (!lf::simt_supported(G, g.head_dim))
+            return fail(LF_ERR_UNSUPPORTED, "CUDA-core kernel not built for G=%d d=%d", G, g.head_dim);
+        c->plan = lf::simt_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+    }
+    if (c->plan.splits < 1 || c->plan.splits > 16)
+        return fail(LF_ERR_UNSUPPORTED, "split plan out of range (%d splits)", c->plan.splits);
+    return LF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lf_status_string(lf_status s) {
+    switch (s) {
+        case LF_OK: return "LF_OK";
+        case LF_ERR_INVALID_ARGUMENT: return "LF_ERR_INVALID_ARGUMENT";
+        case LF_ERR_UNSUPPORTED: return "LF_ERR_UNSUPPORTED";
+        case LF_ERR_OUT_OF_MEMORY: return "LF_ERR_OUT_OF_MEMORY";
+        case LF_ERR_PREFILL_EXCEEDS_BUDGET: return "LF_ERR_PREFILL_EXCEEDS_BUDGET";
+        case LF_ERR_CUDA: return "LF_ERR_CUDA";
+    }
+    return "LF_ERR_UNKNOWN";
+}
+
+const char* lf_last_error(void) { return g_err; }
+
+lf_status lf_cache_bytes(const lf_cache_config* cfg, size_t* bytes) {
+    lf_status s = validate(cfg);
+    if (s) return s;
+    if (!bytes) return fail(LF_ERR_INVALID_ARGUMENT, "bytes is NULL");
+    *bytes = layout_of(*cfg).total;
+    return LF_OK;
+}
+
+lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_buf, size_t buf_bytes,
+                          lf_cache** out) {
+    lf_status s = validate(cfg);
+    if (s) return s;
+    if (!out) return fail(LF_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(LF_ERR_INVALID_ARGUMENT, "device %d of %d", device, ndev);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return cuda_fail(e, "props");
+    if (prop.major != 10) {
+        cudaSetDevice(prev);
+        return fail(LF_ERR_UNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a",
+                    device, prop.major, prop.minor);
+    }
+    lf_cache* c = new (std::nothrow) lf_cache();
+    if (!c) return fail(LF_ERR_OUT_OF_MEMORY, "host allocation");
+    c->cfg = *cfg;
+    if (!(c->cfg.softmax_scale > 0.f)) c->cfg.softmax_scale = 1.0f / sqrtf((float)cfg->head_dim);
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->L = layout_of(c->cfg);
+    if ((s = make_plan(c)) != LF_OK) { delete c; cudaSetDevice(prev); return s; }
+    if (device_buf) {
+        if (buf_bytes < c->L.total || ((uintptr_t)device_buf & 255)) {
+            delete c;
+            cudaSetDevice(prev);
+            return fail(LF_ERR_INVALID_ARGUMENT, "device_buf too small (%zu < %zu) or not 256-aligned",
+                        buf_bytes, c->L.total);
+        }
+        c->slab = device_buf;
+        c->owns = false;
+    } else {
+        e = cudaMalloc(&c->slab, c->L.total);
+        if (e != cudaSuccess) {
+            delete c;
+            cudaSetDevice(prev);
+            cudaGetLastError();
+            return fail(LF_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu): %s", c->L.total, cudaGetErrorString(e));
+        }
+        c->owns = true;
+    }
+    c->slab_bytes = c->L.total;
+    // all slots invalid; zero-filled storage
+    e = cudaMemset(c->slab, 0, c->L.total);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        if (c->owns) cudaFree(c->slab);
+        delete c;
+        return cuda_fail(e, "cache init");
+    }
+    *out = c;
+    return LF_OK;
+}
+
+lf_status lf_cache_destroy(lf_cache* c) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (c->owns) cudaFree(c->slab);
+    cudaSetDevice(prev);
+    delete c;
+    if (e != cudaSuccess) return cuda_fail(e, "destroy");
+    return LF_OK;
+}
+
+lf_status lf_cache_views(const lf_cache* c, void** k, void** v, int32_t** n_valid) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    char* base = (char*)c->slab;
+    if (k) *k = base + c->L.k_off;
+    if (v) *v = base + c->L.v_off;
+    if (n_valid) *n_valid = (int32_t*)(base + c->L.nv_off);
+    return LF_OK;
+}
+
+lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int32_t* split_tokens) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (kernel) *kernel = c->plan.kernel;
+    if (splits) *splits = c->plan.splits;
+    if (split_tokens) *split_tokens = c->plan.chunk;
+    return LF_OK;
+}
+
+int32_t lf_kernels_per_step(const lf_cache* c) { return c ? 1 : 0; }
+
+lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v, int32_t n,
+                          void* stream) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    const lf_cache_config& g = c->cfg;
+    if (seq < 0 || seq >= g.batch) return fail(LF_ERR_INVALID_ARGUMENT, "seq %d of %d", seq, g.batch);
+    if (n < 0) return fail(LF_ERR_INVALID_ARGUMENT, "n < 0");
+    if (n > g.budget)
+        return fail(LF_ERR_PREFILL_EXCEEDS_BUDGET, "prefill exceeds budget; compress first (%d > %d)", n,
+                    g.budget);
+    if (n > 0 && (!k || !v)) return fail(LF_ERR_INVALID_ARGUMENT, "k or v is NULL");
+    cudaStream_t st = (cudaStream_t)stream;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    char* base = (char*)c->slab;
+    size_t row = (size_t)g.head_dim * 2;
+    size_t unit = (size_t)g.budget * row;
+    cudaError_t e = cudaSuccess;
+    if (n > 0) {
+        char* K = base + c->L.k_off + (size_t)seq * g.num_kv_heads * unit;
+        char* V = base + c->L.v_off + (size_t)seq * g.num_kv_heads * unit;
+        e = cudaMemcpy2DAsync(K, unit, k, n * row, n * row, g.num_kv_heads, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(V, unit, v, n * row, n * row, g.num_kv_heads, cudaMemcpyDeviceToDevice, st);
+    }
+    if (e == cudaSuccess) {
+        int32_t* nv = (int32_t*)(base + c->L.nv_off) + (size_t)seq * g.num_kv_heads;
+        fill_i32<<<1, 256, 0, st>>>(nv, n, g.num_kv_heads);
+        e = cudaGetLastError();
+    }
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "prefill");
+    return LF_OK;
+}
+
+lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
+                         int32_t* slot, float* scores, void* stream) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (!q || !k_new || !v_new || !out || !slot)
+        return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new, out and slot must be non-NULL");
+    const lf_cache_config& g = c->cfg;
+    char* base = (char*)c->slab;
+    lf::StepParams p;
+    p.q = (const uint16_t*)q;
+    p.k_new = (const uint16_t*)k_new;
+    p.v_new = (const uint16_t*)v_new;
+    p.K = (uint16_t*)(base + c->L.k_off);
+    p.V = (uint16_t*)(base + c->L.v_off);
+    p.n_valid = (int32_t*)(base + c->L.nv_off);
+    p.out = out;
+    p.slot = slot;
+    p.scores = scores;
+    p.B = g.batch;
+    p.Hq = g.num_q_heads;
+    p.Hkv = g.num_kv_heads;
+    p.G = g.num_q_heads / g.num_kv_heads;
+    p.d = g.head_dim;
+    p.N = g.budget;
+    p.out_f32 = g.out_dtype == LF_DTYPE_F32;
+    p.scale_log2 = (float)((double)g.softmax_scale * 1.4426950408889634);
+    p.splits = c->plan.splits;
+    p.chunk = c->plan.chunk;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != c->device) cudaSetDevice(c->device);
+    cudaError_t e = c->plan.kernel == LF_KERNEL_TCGEN05
+                        ? lf::tc_launch(p, c->plan, (cudaStream_t)stream)
+                        : lf::simt_launch(p, c->plan, (cudaStream_t)stream);
+    if (prev != c->device) cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "decode launch");
+    return LF_OK;
+}
+
+lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new_host,
+                              const void* v_new_host, void* out_host, int32_t* slot_host, void* stream) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (!q_host || !k_new_host || !v_new_host || !out_host || !slot_host)
+        return fail(LF_ERR_INVALID_ARGUMENT, "host buffers must be non-NULL");
+    const lf_cache_config& g = c->cfg;
+    cudaStream_t st = (cudaStream_t)stream;
+    char* base = (char*)c->slab;
+    size_t qb = (size_t)g.batch * g.num_q_heads * g.head_dim * 2;
+    size_t kb = (size_t)g.batch * g.num_kv_heads * g.head_dim * 2;
+    size_t ob = (size_t)g.batch * g.num_q_heads * g.head_dim * (g.out_dtype == LF_DTYPE_F32 ? 4 : 2);
+    size_t sb = (size_t)g.batch * g.num_kv_heads * 4;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaMemcpyAsync(base + c->L.sq_off, q_host, qb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sk_off, k_new_host, kb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sv_off, v_new_host, kb, cudaMemcpyHostToDevice, st);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "h2d");
+    lf_status s = lf_decode_step(c, base + c->L.sq_off, base + c->L.sk_off, base + c->L.sv_off,
+                                 base + c->L.so_off, (int32_t*)(base + c->L.ss_off), nullptr, stream);
+    if (s) return s;
+    cudaSetDevice(c->device);
+    e = cudaMemcpyAsync(out_host, base + c->L.so_off, ob, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(slot_host, base + c->L.ss_off, sb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "d2h");
+    return LF_OK;
+}
+
+}  // extern "C"
