@@ -134,58 +134,79 @@ def dist_env():
 # CPU oracle (cpu_baseline leg / --impl reference): the fp64 oracle as it stands, on host cores
 # ------------------------------------------------------------------------------------------------
 
-def oracle_rate(wl: Workload, B_total: int, seconds: float = 12.0, seed: int = 0):
-    """Times the oracle's same-step decode on a bounded sample of the workload (full caches of
-    a few sequences, all kv heads), extrapolated linearly in units to the full batch (the cost
-    is exactly linear in units).  Returns (tokens/s, cores, sample description, s/step)."""
-    import oracle
-    cores = os.cpu_count() or 1
+class OracleSample:
+    """The fp64 oracle (as it stands) on a bounded sample of the workload: Bs full-cache
+    sequences with all their kv heads, threads = host cores.  Cost is exactly linear in units,
+    so a per-step time scales to the full batch by (B_total / Bs)."""
 
-    def run(Bs, steps):
-        orc = oracle.OracleCache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, nthreads=cores)
+    def __init__(self, wl: Workload, Bs: int, seed: int = 0):
+        import oracle
+        self.wl, self.Bs = wl, Bs
+        self.cores = os.cpu_count() or 1
+        self.orc = oracle.OracleCache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, nthreads=self.cores)
         k, v = random_cache(Bs, wl.Hkv, wl.N, wl.d, seed=seed)
-        orc.K[...] = bits(k)
-        orc.V[...] = bits(v)
-        orc.n_valid[...] = wl.N
-        syn = Synth(Workload(wl.tag, Bs, wl.Hq, wl.Hkv, wl.d, wl.N, 0, steps), seed=seed)
-        ins = [tuple(bits(x) for x in syn.step()) for _ in range(steps)]
+        self.orc.K[...] = bits(k)
+        self.orc.V[...] = bits(v)
+        self.orc.n_valid[...] = wl.N
+        syn = Synth(Workload(wl.tag, Bs, wl.Hq, wl.Hkv, wl.d, wl.N, 0, 8), seed=seed)
+        self.pool = [tuple(bits(x) for x in syn.step()) for _ in range(4)]
+        self.i = 0
+
+    def step(self) -> float:
+        q, kn, vn = self.pool[self.i % len(self.pool)]
+        self.i += 1
         t0 = time.perf_counter()
-        for q, kn, vn in ins:
-            orc.step(q, kn, vn)
+        self.orc.step(q, kn, vn)
         return time.perf_counter() - t0
 
-    t1 = run(1, 1)
-    units_per_s = wl.Hkv / max(t1, 1e-9)
-    Bs = max(1, min(B_total, int(units_per_s * seconds / wl.Hkv / 2)))
-    steps = 2
-    t = run(Bs, steps)
-    sec_per_unit_step = t / (Bs * wl.Hkv * steps)
-    sec_per_step = sec_per_unit_step * B_total * wl.Hkv
-    desc = (f"{Bs} sequences x {wl.Hkv} kv heads x {steps} steps of workload '{wl.tag}' "
-            f"(full cache N={wl.N}), {t:.1f} s on {cores} threads, extrapolated linearly to batch {B_total}")
-    return B_total / sec_per_step, cores, desc, sec_per_step
+
+def oracle_sample(wl: Workload, B_total: int, seconds_per_step: float, seed: int = 0) -> OracleSample:
+    """Grows the sample (x4 sequences at a time, capped at the batch) until one oracle step over
+    it takes about `seconds_per_step`."""
+    Bs = 1
+    smp = OracleSample(wl, Bs, seed)
+    t = smp.step()
+    while t < seconds_per_step / 2 and Bs < B_total:
+        Bs = min(B_total, max(Bs + 1, int(Bs * min(4.0, seconds_per_step / max(t, 1e-6)))))
+        smp = OracleSample(wl, Bs, seed)
+        t = smp.step()
+    return smp
+
+
+def describe(smp: OracleSample, steps: int, B_total: int) -> str:
+    return (f"{smp.Bs} of {B_total} sequences x {smp.wl.Hkv} kv heads (full cache N={smp.wl.N}) of workload "
+            f"'{smp.wl.tag}', {steps} timed oracle steps on {smp.cores} threads, per-step time scaled "
+            f"linearly by {B_total}/{smp.Bs} units to the whole batch")
+
+
+def oracle_rate(wl: Workload, B_total: int, seconds: float = 12.0, seed: int = 0):
+    """cpu_baseline leg: ~`seconds` of oracle time.  Returns (tokens/s, cores, sample, s/step)."""
+    smp = oracle_sample(wl, B_total, seconds / 4, seed)
+    ts = [smp.step() for _ in range(3)]
+    sps = float(np.median(ts)) * B_total / smp.Bs
+    return B_total / sps, smp.cores, describe(smp, 3, B_total), sps
 
 
 def run_reference(args, wl, B_total):
+    """--impl reference: the oracle on the host cores, same workload/metric/unit as our arm;
+    each step is a bounded sample so the whole W+K run stays within a few minutes."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    vals = []
-    descs = None
-    for _ in range(max(args.warmup, 0)):
-        pass   # the oracle has no warm-up state; each timed step is a fresh bounded sample
-    for _ in range(args.steps):
-        v, cores, desc, sps = oracle_rate(wl, B_total, seconds=args.ref_seconds)
-        vals.append(v)
-        descs = (cores, desc, sps)
-    value = float(np.median(vals))
-    cores, desc, sps = descs
+    per_step = max(0.05, min(args.ref_seconds, 150.0 / (args.steps + args.warmup)))
+    smp = oracle_sample(wl, B_total, per_step, args.seed)
+    for _ in range(args.warmup):
+        smp.step()
+    ts = [smp.step() for _ in range(args.steps)]
+    sps = float(np.median(ts)) * B_total / smp.Bs
+    value = B_total / sps
+    desc = describe(smp, args.steps, B_total)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sps * 1e3, "higher_is_better": True,
         "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_of(args, wl, B_total, None),
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": smp.cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
