@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "liblongflow.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in
            ("lf_runtime.cu", "lf_decode_simt.cu", "lf_decode_tc.cu")]
-HEADERS = [os.path.join(HERE, "csrc", "lf_internal.h"), os.path.join(HERE, "csrc", "lf_tc_ptx.cuh"),
+HEADERS = [os.path.join(HERE, "csrc", f) for f in ("lf_internal.h", "lf_tc_ptx.cuh", "lf_common.cuh")] + [
            os.path.join(ROOT, "include", "longflow.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -20,11 +20,7 @@
 //           lowest index on exact ties (R7).
 //   write   rank 0: out = (sum_s o_s 2^(m_s - M) + 2^(x* - M) v*) / Z, slot, in-place eviction
 //           write of (k*, v*) into the victim (Fig. 2) or append at n (R11).
-#include <cooperative_groups.h>
-
-#include "lf_internal.h"
-
-namespace cg = cooperative_groups;
+#include "lf_common.cuh"
 
 namespace lf {
 namespace {
@@ -73,18 +69,6 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& w, float* f) {
     f[4] = __uint_as_float(w.z << 16); f[5] = __uint_as_float(w.z & 0xffff0000u);
     f[6] = __uint_as_float(w.w << 16); f[7] = __uint_as_float(w.w & 0xffff0000u);
 }
-__device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float(((uint32_t)b) << 16); }
-__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
-    uint32_t u = __float_as_uint(f);
-    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40);  // quiet NaN
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return (uint16_t)(u >> 16);
-}
-// fp32 -> uint32 whose unsigned order is the float order (for the argmin key)
-__device__ __forceinline__ uint32_t ordered_bits(float f) {
-    uint32_t u = __float_as_uint(f);
-    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
-}
 
 // Stage one tile (vt valid rows starting at slot j0) of a unit's K or V into swizzled SMEM:
 // 16-byte chunk c of row r lives at chunk position c ^ (r & 7) of that row.
@@ -112,11 +96,7 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
     float* ex_z = (float*)(smem + so.exch_z);
     float* ex_o = (float*)(smem + so.exch_o);
     float* misc = (float*)(smem + so.misc);
-    float* xnew = misc;            // [16]
-    float* gM = misc + 16;         // [16]
-    float* glz = misc + 32;        // [16]
-    float* gZ = misc + 48;         // [16]
-    float* wred = misc + 64;       // [64] per-warp reduction slots
+    float* wred = misc + 64;       // [64] per-warp reduction slots (misc[0,64) is the finaliser's)
     unsigned long long* keys = (unsigned long long*)(smem + so.key);
     float* X = (float*)(smem + so.X);
     float* Ls = (float*)(smem + so.L);
@@ -294,113 +274,9 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
             const int g = tid, k = g / 4, w = 2 * (g % 4);
             ex_z[g] = wred[w * 4 + k] + wred[(w + 1) * 4 + k];
         }
-        // current token's logit x_g* (computed identically by every CTA of the cluster)
-        const uint16_t* kn = p.k_new + (size_t)u * D;
-        for (int g = warp; g < G; g += 8) {
-            float acc = 0.f;
-            for (int l = lane; l < D; l += 32) acc = fmaf(qs[g * D + l], bf16_to_f32(kn[l]), acc);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) xnew[g] = acc * p.scale_log2;
-        }
     }
-    cluster.sync();   // #1: every CTA's (m, Z, o) partials are visible cluster-wide
-    // ---------------- global M_g, Z_g (same order in every CTA) ----------------------------
-    if (tid < G) {
-        const int g = tid;
-        float M = xnew[g];
-        for (int r = 0; r < S; ++r) M = fmaxf(M, cluster.map_shared_rank(ex_m, r)[g]);
-        float Z = 0.f;
-        for (int r = 0; r < S; ++r) {
-            const float mr = cluster.map_shared_rank(ex_m, r)[g];
-            const float zr = cluster.map_shared_rank(ex_z, r)[g];
-            Z += zr * exp2f(mr - M);
-        }
-        Z += exp2f(xnew[g] - M);
-        gM[g] = M;
-        gZ[g] = Z;
-        glz[g] = log2f(Z);
-    }
-    __syncthreads();
-    // ---------------- scores + local argmin ------------------------------------------------
-    unsigned long long best = ~0ull;
-    const float log2G = log2f((float)G);
-    for (int j = tid; j < nv; j += kNT) {
-        const float lam = Ls[j];
-        float a[GP];
-        float amax = -INFINITY;
-#pragma unroll
-        for (int g = 0; g < GP; ++g) {
-            a[g] = g < G ? X[g * chunk + j] - gM[g] - glz[g] : -INFINITY;
-            amax = fmaxf(amax, a[g]);
-        }
-        float ssum = 0.f;
-#pragma unroll
-        for (int g = 0; g < GP; ++g) ssum += exp2f(a[g] - amax);
-        const float ls = log2f(lam) + amax + log2f(ssum) - log2G;   // log2 I_j
-        if (p.scores) {
-            float sc = 0.f;
-#pragma unroll
-            for (int g = 0; g < GP; ++g) sc += exp2f(a[g]);
-            p.scores[(size_t)u * N + c0 + j] = lam * sc / (float)G;
-        }
-        const unsigned long long key = ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(c0 + j);
-        best = key < best ? key : best;
-    }
-    if (p.scores)
-        for (int j = nv + tid; j < c1 - c0; j += kNT) p.scores[(size_t)u * N + c0 + j] = INFINITY;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        unsigned long long o2 = __shfl_xor_sync(0xffffffffu, best, off);
-        best = o2 < best ? o2 : best;
-    }
-    if (lane == 0) keys[1 + warp] = best;
-    __syncthreads();
-    if (tid == 0) {
-        unsigned long long m = keys[1];
-        for (int w = 1; w < 8; ++w) m = keys[1 + w] < m ? keys[1 + w] : m;
-        keys[0] = m;
-    }
-    cluster.sync();   // #2: per-CTA argmin keys visible
-    if (s == 0) {
-        __shared__ int s_slot;
-        if (tid == 0) {
-            unsigned long long m = ~0ull;
-            for (int r = 0; r < S; ++r) {
-                unsigned long long kr = cluster.map_shared_rank(keys, r)[0];
-                m = kr < m ? kr : m;
-            }
-            int sl = n < N ? n : (int)(m & 0xffffffffull);
-            s_slot = sl;
-            p.slot[u] = sl;
-            if (n < N) p.n_valid[u] = n + 1;
-        }
-        __syncthreads();
-        const int sl = s_slot;
-        // output: combine the partial accumulators of every split + the current token
-        const uint16_t* vn = p.v_new + (size_t)u * D;
-        for (int i = tid; i < G * D; i += kNT) {
-            const int g = i / D, l = i % D;
-            float acc = 0.f;
-            for (int r = 0; r < S; ++r) {
-                const float mr = cluster.map_shared_rank(ex_m, r)[g];
-                acc += cluster.map_shared_rank(ex_o, r)[g * D + l] * exp2f(mr - gM[g]);
-            }
-            acc += exp2f(xnew[g] - gM[g]) * bf16_to_f32(vn[l]);
-            const float ov = acc / gZ[g];
-            const size_t oi = ((size_t)b * p.Hq + (size_t)h * G + g) * D + l;
-            if (p.out_f32) ((float*)p.out)[oi] = ov;
-            else ((uint16_t*)p.out)[oi] = f32_to_bf16_rne(ov);
-        }
-        // in-place eviction write (or append): every CTA finished reading K/V before sync #1
-        if (tid < D / 8) {
-            const uint4* ks = (const uint4*)(p.k_new + (size_t)u * D);
-            const uint4* vs = (const uint4*)(p.v_new + (size_t)u * D);
-            ((uint4*)(p.K + unit_off + (size_t)sl * D))[tid] = ks[tid];
-            ((uint4*)(p.V + unit_off + (size_t)sl * D))[tid] = vs[tid];
-        }
-    }
-    cluster.sync();   // #3: rank 0 is done reading remote shared memory
+    Partials pt{ex_m, ex_z, ex_o, X, Ls, misc, keys};
+    cluster_finalize<D, GP, kNT>(p, pt, u, n, c0, c1, nv);
 }
 
 template <int D, int GP>

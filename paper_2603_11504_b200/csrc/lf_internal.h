@@ -38,8 +38,13 @@ Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms);
 cudaError_t simt_launch(const StepParams& p, const Plan& plan, cudaStream_t stream);
 
 // TMA + tcgen05 split-KV kernel (lf_decode_tc.cu)
+struct TcMaps {               // two CUtensorMap (K, V) encoded once per cache (the slab is static)
+    alignas(64) unsigned char k[128];
+    alignas(64) unsigned char v[128];
+};
 bool tc_supported(int G, int d);
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms);
-cudaError_t tc_launch(const StepParams& p, const Plan& plan, cudaStream_t stream);
+bool tc_make_maps(TcMaps* maps, void* K, void* V, long long units, int N, int d);
+cudaError_t tc_launch(const StepParams& p, const Plan& plan, const TcMaps& maps, cudaStream_t stream);
 
 }  // namespace lf

@@ -98,6 +98,7 @@ struct lf_cache {
     bool owns;
     Layout L;
     lf::Plan plan;
+    lf::TcMaps maps;
 };
 
 namespace {
@@ -196,6 +197,14 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
         c->owns = true;
     }
     c->slab_bytes = c->L.total;
+    if (c->plan.kernel == LF_KERNEL_TCGEN05 &&
+        !lf::tc_make_maps(&c->maps, (char*)c->slab + c->L.k_off, (char*)c->slab + c->L.v_off,
+                          (long long)cfg->batch * cfg->num_kv_heads, cfg->budget, cfg->head_dim)) {
+        if (c->owns) cudaFree(c->slab);
+        delete c;
+        cudaSetDevice(prev);
+        return fail(LF_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K/V tensor maps");
+    }
     // all slots invalid; zero-filled storage
     e = cudaMemset(c->slab, 0, c->L.total);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
@@ -307,7 +316,7 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);
     cudaError_t e = c->plan.kernel == LF_KERNEL_TCGEN05
-                        ? lf::tc_launch(p, c->plan, (cudaStream_t)stream)
+                        ? lf::tc_launch(p, c->plan, c->maps, (cudaStream_t)stream)
                         : lf::simt_launch(p, c->plan, (cudaStream_t)stream);
     if (prev != c->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
