@@ -25,6 +25,13 @@ __device__ __forceinline__ uint32_t ordered_bits(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// explicit shared-state-space accesses for pointers the compiler only sees as generic
+__device__ __forceinline__ float lds_f32(const float* p) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) {
     return a < b ? a : b;
 }
@@ -95,12 +102,12 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
     const float log2G = log2f((float)G);
     const float invG = 1.0f / (float)G;
     for (int j = tid; j < nv; j += NT) {
-        const float lam = t.L[j];
+        const float lam = lds_f32(t.L + j);
         float a[GP];
         float amax = -INFINITY;
 #pragma unroll
         for (int g = 0; g < GP; ++g) {
-            a[g] = g < G ? t.X[g * chunk + j] - gM[g] - glz[g] : -INFINITY;
+            a[g] = g < G ? lds_f32(t.X + g * chunk + j) - gM[g] - glz[g] : -INFINITY;
             amax = fmaxf(amax, a[g]);
         }
         float ssum = 0.f, sc = 0.f;

@@ -75,8 +75,9 @@ template <int GP>
 __global__ void __launch_bounds__(kNT, 2) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ unsigned char smem_raw[];
     const StepParams& p = a.p;
-    unsigned char* smem =
-        (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);   // swizzle-128B atoms
+    // 1024-byte aligned base for the swizzle-128B atoms; offset arithmetic on the __shared__
+    // pointer keeps the accesses in the shared state space (STS/LDS, not generic ST/LD)
+    unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int G = p.G, N = p.N, chunk = p.chunk;
     const TcSmem so = tc_smem(G, GP, chunk);
     float* X = (float*)(smem + so.X);
