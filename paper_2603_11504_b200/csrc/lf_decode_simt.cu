@@ -320,6 +320,8 @@ bool simt_supported(int G, int d) { return G >= 1 && G <= 8 && (d == 64 || d == 
 Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     Plan pl;
     pl.kernel = LF_KERNEL_SIMT;
+    pl.clusters = 0;
+    pl.stages = 2;
     const int GP = gpad(G);
     const int fixed = simt_smem(d, GP, G, 0).total;
     int chunk_max = (kMaxSmem - fixed) / ((G + 1) * 4) / 128 * 128;

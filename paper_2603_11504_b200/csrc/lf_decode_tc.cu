@@ -1,21 +1,27 @@
-// TMA + tcgen05 split-KV LongFlow decode step for head_dim 128 and 2 <= G <= 8 (B200, sm_100a).
+// TMA + tcgen05 persistent split-KV LongFlow decode step, head_dim 128, 2 <= G <= 8 (B200, sm_100a).
 //
-// One thread-block cluster per unit u = (sequence, kv head); CTA s owns slots [s*chunk, (s+1)*chunk)
-// and streams them in 128-token tiles (K tiles first, then V tiles) through a 2-stage TMA ring
-// (SWIZZLE_128B, two 64-column boxes per tile).  Warp roles (192 threads):
-//   warp 0     TMA producer (one elected lane)
+// Grid = C persistent clusters of S CTAs (1 CTA per SM).  Cluster c handles units
+// u = c, c + C, c + 2C, ... (unit = (sequence, kv head)); CTA s of the cluster owns slots
+// [s*chunk, (s+1)*chunk) of every unit.  Warp roles (192 threads):
+//   warp 0     producer: Q rows of the next unit (LDG -> swizzled SMEM) and the K then V tiles
+//              (128 tokens x 128 d, two SWIZZLE_128B TMA boxes) through an ST-stage ring
 //   warp 1     TMEM allocator + tcgen05.mma issuer (one lane)
-//   warps 2-5  softmax / score / epilogue warps; warp w owns TMEM lanes [32(w%4), 32(w%4)+32)
+//   warps 2-5  softmax / score / exchange warps; warp w owns TMEM lanes [32(w%4), 32(w%4)+32)
+// The producer and MMA warps run ahead into the next unit while the softmax warps finish the
+// current one, so the HBM stream does not drain at unit boundaries.
 //
-// K pass   S^T[128 tok x 16] = K_tile[128 x 128] . Q^T[128 x 16]  (M=128, N=16, K=128; K-major A/B),
-//          fp32 in TMEM (double buffered); the softmax warps move x_gj = S*scale*log2e to SMEM
-//          (Alg. 1) and track the exact per-CTA max (R5).
-// V pass   P_g = 2^(x_g - m_g) split into bf16 hi + lo (N = 16 = 8 hi rows + 8 lo rows: bf16 P alone
-//          misses the 2e-3 output bar), O^T[128 d x 16] += V^T[d x 128 tok] . P^T
-//          (M=128, N=16, K=16 per MMA, A MN-major straight from the TMA tile); lambda_j = ||v_j||_1
-//          from the same tile on the CUDA cores (Eq. 6, R9).  Invalid rows of the last tile are
-//          zeroed in SMEM before the MMA reads them.
-// Then the shared cluster finalisation (lf_common.cuh): DSMEM combine, scores, argmin, eviction.
+// Per unit (Alg. 1 P:500-547 restructured):
+//   K pass  S^T[128 tok x 16] = K_tile . Q^T (M=128, N=16, K=128, both K-major), fp32 in TMEM
+//           (double buffered); x_gj = S * scale * log2e -> SMEM, exact per-CTA max m_g (R5).
+//   V pass  P_g = 2^(x_g - m_g) as bf16 hi + lo (N = 16: 8 hi rows + 8 lo rows; bf16 P alone
+//           misses the 2e-3 out bar); O^T[128 d x 16] += V^T . P^T (M=128, N=16,
+//           K=16 tokens per MMA, A MN-major straight from the TMA tile); lambda_j = ||v_j||_1 from
+//           the same tile on the CUDA cores (Eq. 6, R9).  Rows past n are zeroed first.
+//   exchange (no cluster-wide barrier): each CTA publishes (m_g, Z_g, o_g) in its SMEM and
+//           arrives on every rank's `xready` mbarrier; after reading all (m, Z) it computes
+//           M_g, Z_g (incl. the current token), its scores and argmin key, arrives on rank 0's
+//           `kready`; rank 0 picks the slot (lowest index on ties), combines o, writes out,
+//           evicts in place (Fig. 2); `xfree` arrivals release the buffers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -25,44 +31,57 @@
 namespace lf {
 namespace {
 
-constexpr int kStages = 2;
 constexpr int kNT = 192;
 constexpr int kStageBytes = 32768;   // 128 tokens x 128 d x bf16 (two 16 KB boxes)
 constexpr int kBoxBytes = 16384;
-constexpr int kMaxSmem = 110 * 1024; // two CTAs per SM
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMaxStages = 6;
 constexpr uint32_t kTmemCols = 64;   // S double buffer (2 x 16) + O (16), power of two
 
 struct TcArgs {
     CUtensorMap tmK;
     CUtensorMap tmV;
     StepParams p;
+    int32_t clusters;   // C: persistent clusters in the grid
+    int32_t stages;     // ring depth
+};
+
+// exchange buffer, one per unit parity
+struct Xchg {
+    float m[16];
+    float z[16];
+    unsigned long long key;
+    unsigned long long pad;
+    float o[8 * 128];   // [GP][128], un-normalised
 };
 
 struct TcSmem {
-    int ring, q, pbuf, X, L, exo, exm, exz, misc, keys, red, bars, tmem, total;
+    int ring, q, pbuf, X, L, xb, misc, red, bars, tmem, total;
 };
-__host__ __device__ inline TcSmem tc_smem(int G, int GP, int chunk) {
+__host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
     TcSmem s;
     int off = 0;
-    s.ring = off; off += kStages * kStageBytes;   // 1024-aligned (swizzle atoms)
-    s.q = off;    off += 4096;                    // Q^T operand: 16 rows x 128 d, 2 boxes of 2 KB
-    s.pbuf = off; off += 2 * 4096;                // P^T operand, double buffered: 16 rows x 128 tok
-    s.X = off;    off += G * chunk * 4;
-    s.L = off;    off += chunk * 4;
-    s.exo = off;  off += GP * 128 * 4;
-    s.exm = off;  off += 64;
-    s.exz = off;  off += 64;
+    s.ring = off; off += stages * kStageBytes;   // 1024-aligned (swizzle atoms)
+    s.q = off;    off += 2 * 4096;               // Q^T operand x2 (per unit parity): 16 rows x 128 d
+    s.pbuf = off; off += 2 * 4096;               // P^T operand x2: 16 rows x 128 tokens
+    s.X = off;    off += G * chunk * 4;          // x_gj of the current unit
+    s.L = off;    off += chunk * 4;              // lambda_j of the current unit
+    s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 128 * 4;
-    s.keys = off; off += 16 * 8;
-    s.red = off;  off += 2 * 4 * 16 * 4;
-    s.bars = off; off += 16 * 8;
+    s.red = off;  off += 3 * 4 * 16 * 4;
+    s.bars = off; off += 40 * 8;
     s.tmem = off; off += 16;
-    s.total = off + 1024;                         // slack for 1024-byte alignment of the base
+    s.total = off + 1024;                        // slack for 1024-byte alignment of the base
     return s;
 }
 
-// barrier slots
-constexpr int FULL = 0, EMPTY = 2, SFULL = 4, SFREE = 6, PREADY = 8, PFREE = 10, OFULL = 12;
+// mbarrier slots
+constexpr int FULL = 0;                 // [kMaxStages]
+constexpr int EMPTY = FULL + kMaxStages;
+constexpr int SFULL = EMPTY + kMaxStages, SFREE = SFULL + 2, PREADY = SFREE + 2, PFREE = PREADY + 2;
+constexpr int QFULL = PFREE + 2, QFREE = QFULL + 2, OFULL = QFREE + 2, OFREE = OFULL + 1;
+constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
+static_assert(NBARS <= 40, "barrier slots");
 
 __device__ __forceinline__ float habs_sum8(const uint4& w) {
     return (fabsf(__uint_as_float(w.x << 16)) + fabsf(__uint_as_float(w.x & 0xffff0000u))) +
@@ -71,25 +90,37 @@ __device__ __forceinline__ float habs_sum8(const uint4& w) {
            (fabsf(__uint_as_float(w.w << 16)) + fabsf(__uint_as_float(w.w & 0xffff0000u)));
 }
 
+struct UnitInfo {
+    int u, b, h, n, c0, c1, nv, ntiles;
+};
+__device__ __forceinline__ UnitInfo unit_info(const StepParams& p, int u, int s) {
+    UnitInfo x;
+    x.u = u;
+    x.b = u / p.Hkv;
+    x.h = u % p.Hkv;
+    x.n = __ldcg(p.n_valid + u);
+    x.c0 = s * p.chunk;
+    x.c1 = min(x.c0 + p.chunk, p.N);
+    x.nv = max(0, min(x.c1, x.n) - x.c0);
+    x.ntiles = (x.nv + 127) / 128;
+    return x;
+}
+
 template <int GP>
-__global__ void __launch_bounds__(kNT, 2) tc_decode_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ unsigned char smem_raw[];
     const StepParams& p = a.p;
-    // 1024-byte aligned base for the swizzle-128B atoms; offset arithmetic on the __shared__
-    // pointer keeps the accesses in the shared state space (STS/LDS, not generic ST/LD)
+    // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int G = p.G, N = p.N, chunk = p.chunk;
-    const TcSmem so = tc_smem(G, GP, chunk);
+    const int G = p.G, N = p.N, chunk = p.chunk, ST = a.stages;
+    const TcSmem so = tc_smem(G, chunk, ST);
     float* X = (float*)(smem + so.X);
     float* Ls = (float*)(smem + so.L);
-    float* ex_o = (float*)(smem + so.exo);
-    float* ex_m = (float*)(smem + so.exm);
-    float* ex_z = (float*)(smem + so.exz);
+    Xchg* xb = (Xchg*)(smem + so.xb);
     float* misc = (float*)(smem + so.misc);
     float* red = (float*)(smem + so.red);
-    unsigned long long* keys = (unsigned long long*)(smem + so.keys);
     const uint32_t ring = ptx::smem_u32(smem + so.ring);
-    const uint32_t qs = ptx::smem_u32(smem + so.q);
+    const uint32_t qsm = ptx::smem_u32(smem + so.q);
     const uint32_t pbuf = ptx::smem_u32(smem + so.pbuf);
     const uint32_t bars = ptx::smem_u32(smem + so.bars);
     auto BAR = [&](int i) { return bars + 8u * (uint32_t)i; };
@@ -97,17 +128,13 @@ __global__ void __launch_bounds__(kNT, 2) tc_decode_kernel(const __grid_constant
     cg::cluster_group cluster = cg::this_cluster();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = p.splits;
-    const int u = blockIdx.x / S;
     const int s = (int)cluster.block_rank();
-    const int b = u / p.Hkv, h = u % p.Hkv;
-    const int n = p.n_valid[u];
-    const int c0 = s * chunk;
-    const int c1 = min(c0 + chunk, N);
-    const int nv = max(0, min(c1, n) - c0);
-    const int ntiles = (nv + 127) / 128;
+    const int cid = blockIdx.x / S;
+    const int C = a.clusters;
+    const int units = p.B * p.Hkv;
 
     if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) {
+        for (int i = 0; i < ST; ++i) {
             ptx::mbar_init(BAR(FULL + i), 1);      // producer's expect_tx arrival
             ptx::mbar_init(BAR(EMPTY + i), 5);     // MMA commit + 4 softmax warps
         }
@@ -116,247 +143,435 @@ __global__ void __launch_bounds__(kNT, 2) tc_decode_kernel(const __grid_constant
             ptx::mbar_init(BAR(SFREE + i), 4);
             ptx::mbar_init(BAR(PREADY + i), 4);
             ptx::mbar_init(BAR(PFREE + i), 1);
+            ptx::mbar_init(BAR(QFULL + i), 1);
+            ptx::mbar_init(BAR(QFREE + i), 1);
+            ptx::mbar_init(BAR(XREADY + i), S);    // one arrival per rank
+            ptx::mbar_init(BAR(KREADY + i), S);
+            ptx::mbar_init(BAR(XFREE + i), S);
         }
         ptx::mbar_init(BAR(OFULL), 1);
+        ptx::mbar_init(BAR(OFREE), 4);
         ptx::fence_mbar_init();
         ptx::tma_prefetch_desc(&a.tmK);
         ptx::tma_prefetch_desc(&a.tmV);
     }
     if (warp == 1) ptx::tmem_alloc<kTmemCols>(ptx::smem_u32(smem + so.tmem));
-    if (warp >= 2) {
-        // Q^T as the K-major SW128 B operand: row n (query head, zero for n >= G), column k (d);
-        // 16-byte chunk (k%64)/8 of row n sits at chunk position ((k%64)/8) ^ (n%8)
-        const int sidx = tid - 64;
-        uint16_t* qsm = (uint16_t*)(smem + so.q);
-        for (int e = sidx; e < 16 * 128; e += 128) {
-            const int row = e >> 7, col = e & 127, cc = col & 63;
-            const uint16_t v = row < G ? p.q[((size_t)b * p.Hq + (size_t)h * G + row) * 128 + col] : (uint16_t)0;
-            qsm[((col >> 6) * 2048 + row * 128 + ((((cc >> 3) ^ (row & 7)) << 4)) + (cc & 7) * 2) >> 1] = v;
-        }
-        uint4* pz = (uint4*)(smem + so.pbuf);
-        for (int e = sidx; e < 2 * 4096 / 16; e += 128) pz[e] = make_uint4(0, 0, 0, 0);
+    if (warp >= 2) {   // zero both Q and both P operand buffers (rows >= G stay zero)
+        uint4* z = (uint4*)(smem + so.q);
+        for (int e = tid - 64; e < 4 * 4096 / 16; e += 128) z[e] = make_uint4(0, 0, 0, 0);
         ptx::fence_proxy_async_smem();
     }
     ptx::tc_fence_before();
-    __syncthreads();
+    ptx::cluster_sync_all();   // barriers of every rank initialised before any remote arrival
     ptx::tc_fence_after();
     const uint32_t tmem = *(volatile uint32_t*)(smem + so.tmem);
 
     if (warp == 0) {
-        // ------------------------------ TMA producer ------------------------------------------
-        if (lane == 0) {
-            for (int i = 0; i < 2 * ntiles; ++i) {
-                const int st = i % kStages;
-                const uint32_t ph = (uint32_t)(i / kStages) & 1u;
-                ptx::mbar_wait(BAR(EMPTY + st), ph ^ 1u);
-                ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
-                const int tile = i < ntiles ? i : i - ntiles;
-                const int row = u * N + c0 + tile * 128;
-                const void* tm = i < ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
-                const uint32_t dst = ring + (uint32_t)st * kStageBytes;
-                ptx::tma_load_2d(dst, tm, BAR(FULL + st), 0, row);
-                ptx::tma_load_2d(dst + kBoxBytes, tm, BAR(FULL + st), 64, row);
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        // ------------------------------ MMA issuer --------------------------------------------
-        if (lane == 0) {
-            constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 16, 0, 0);
-            constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
-            for (int i = 0; i < ntiles; ++i) {          // S^T = K_tile . Q^T
-                const int st = i % kStages;
-                ptx::mbar_wait(BAR(FULL + st), (uint32_t)(i / kStages) & 1u);
-                const int sb = i & 1;
-                ptx::mbar_wait(BAR(SFREE + sb), ((uint32_t)(i >> 1) & 1u) ^ 1u);
-                ptx::tc_fence_after();
-                const uint32_t base = ring + (uint32_t)st * kStageBytes;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t da = ptx::smem_desc_sw128(base + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
-                    const uint64_t db = ptx::smem_desc_sw128(qs + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                    ptx::mma_bf16(tmem + (uint32_t)sb * 16, da, db, idesc_qk, kk > 0);
-                }
-                ptx::mma_commit(BAR(SFULL + sb));
-                ptx::mma_commit(BAR(EMPTY + st));
-            }
-            for (int i = 0; i < ntiles; ++i) {          // O^T += V^T . P^T
-                const int j = ntiles + i, st = j % kStages;
-                ptx::mbar_wait(BAR(FULL + st), (uint32_t)(j / kStages) & 1u);
-                const int pb = i & 1;
-                ptx::mbar_wait(BAR(PREADY + pb), (uint32_t)(i >> 1) & 1u);
-                ptx::tc_fence_after();
-                const uint32_t base = ring + (uint32_t)st * kStageBytes;
-                const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const uint64_t da = ptx::smem_desc_sw128(base + kk * 2048, kBoxBytes, 1024);
-                    const uint64_t db = ptx::smem_desc_sw128(pbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                    ptx::mma_bf16(tmem + 32, da, db, idesc_pv, (i | kk) > 0);
-                }
-                ptx::mma_commit(BAR(EMPTY + st));
-                ptx::mma_commit(BAR(PFREE + pb));
-            }
-            ptx::mma_commit(BAR(OFULL));
-        }
-        __syncwarp();
-    } else {
-        // ------------------------------ softmax / score warps ----------------------------------
-        const int q4 = warp & 3;
-        const int row = 32 * q4 + lane;                 // TMEM lane = token row of the tile / d index
-        const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
-        float mloc[GP];
-#pragma unroll
-        for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
-        for (int i = 0; i < ntiles; ++i) {
-            const int st = i % kStages, sb = i & 1;
-            ptx::mbar_wait(BAR(SFULL + sb), (uint32_t)(i >> 1) & 1u);
-            ptx::tc_fence_after();
-            uint32_t r[8];
-            ptx::tmem_ld_x8(tl + (uint32_t)sb * 16, r);
-            ptx::tmem_ld_wait();
-            const int tok = i * 128 + row;
-            const bool valid = tok < nv;
-#pragma unroll
-            for (int g = 0; g < GP; ++g) {
-                if (g < G) {
-                    const float x = valid ? __uint_as_float(r[g]) * p.scale_log2 : -INFINITY;
-                    X[g * chunk + tok] = x;
-                    mloc[g] = fmaxf(mloc[g], x);
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                ptx::mbar_arrive(BAR(SFREE + sb));
-                ptx::mbar_arrive(BAR(EMPTY + st));
-            }
-        }
-        // exact per-CTA max over the 128 softmax threads
-#pragma unroll
-        for (int g = 0; g < GP; ++g) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) mloc[g] = fmaxf(mloc[g], __shfl_xor_sync(0xffffffffu, mloc[g], off));
-        }
-        if (lane == 0) {
-#pragma unroll
-            for (int g = 0; g < GP; ++g) red[q4 * 16 + g] = mloc[g];
-        }
-        ptx::named_bar_sync(1, 128);
-        float m[GP];
-#pragma unroll
-        for (int g = 0; g < GP; ++g)
-            m[g] = fmaxf(fmaxf(red[0 * 16 + g], red[1 * 16 + g]), fmaxf(red[2 * 16 + g], red[3 * 16 + g]));
-        if (tid == 64) {
-#pragma unroll
-            for (int g = 0; g < GP; ++g)
-                if (g < G) ex_m[g] = m[g];
-        }
-        float z[GP];
-#pragma unroll
-        for (int g = 0; g < GP; ++g) z[g] = 0.f;
-        const int box = row >> 6, cc = row & 63;
-        for (int i = 0; i < ntiles; ++i) {
-            const int pb = i & 1;
-            ptx::mbar_wait(BAR(PFREE + pb), ((uint32_t)(i >> 1) & 1u) ^ 1u);
-            const int tok = i * 128 + row;
-            const bool valid = tok < nv;
-            unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
-#pragma unroll
-            for (int g = 0; g < GP; ++g) {
-                if (g < G) {
-                    const float pv = valid ? exp2f(X[g * chunk + tok] - m[g]) : 0.f;
-                    z[g] += pv;
-                    const uint16_t hi = f32_to_bf16_rne(pv);
-                    const uint16_t lo = f32_to_bf16_rne(pv - bf16_to_f32(hi));
-                    *(uint16_t*)(P + g * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = hi;
-                    *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ (8 + g)) & 7) << 4) + (cc & 7) * 2) = lo;
-                }
-            }
-            const int j = ntiles + i, st = j % kStages;
-            ptx::mbar_wait(BAR(FULL + st), (uint32_t)(j / kStages) & 1u);   // V tile landed
-            unsigned char* Vt = smem + so.ring + st * kStageBytes;
-            if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
-#pragma unroll
-                for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        *(uint4*)(Vt + bb * kBoxBytes + row * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+        // ------------------------------ producer -------------------------------------------------
+        uint32_t it = 0, qi = 0;
+        for (int u = cid; u < units; u += C, ++qi) {
+            const UnitInfo x = unit_info(p, u, s);
+            const int qb = qi & 1;
+            ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
+            // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ (g%8) of box c/8
+            const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
+            unsigned char* qd = smem + so.q + qb * 4096;
+            for (int e = lane; e < G * 16; e += 32) {
+                const int g = e >> 4, c = e & 15;
+                *(uint4*)(qd + (c >> 3) * 2048 + g * 128 + (((c & 7) ^ (g & 7)) << 4)) = __ldg(qg + e);
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
-            float lam = 0.f;
-            if (valid) {
-#pragma unroll
-                for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((c ^ (row & 7)) << 4)));
+            if (lane == 0) {
+                ptx::mbar_arrive(BAR(QFULL + qb));
+                for (int i = 0; i < 2 * x.ntiles; ++i, ++it) {
+                    const int st = it % ST;
+                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                    ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
+                    const int tile = i < x.ntiles ? i : i - x.ntiles;
+                    const int row = u * N + x.c0 + tile * 128;
+                    const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
+                    const uint32_t dst = ring + (uint32_t)st * kStageBytes;
+                    ptx::tma_load_2d(dst, tm, BAR(FULL + st), 0, row);
+                    ptx::tma_load_2d(dst + kBoxBytes, tm, BAR(FULL + st), 64, row);
+                }
             }
-            Ls[tok] = lam;
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(BAR(EMPTY + st));
+            it = __shfl_sync(0xffffffffu, it, 0);
         }
-        // Z over the 128 softmax threads (fixed order)
-#pragma unroll
-        for (int g = 0; g < GP; ++g) {
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) z[g] += __shfl_xor_sync(0xffffffffu, z[g], off);
-        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer -----------------------------------------------
         if (lane == 0) {
+            constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 16, 0, 0);
+            constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
+            uint32_t it = 0, si = 0, pi = 0, ui = 0;
+            for (int u = cid; u < units; u += C, ++ui) {
+                const UnitInfo x = unit_info(p, u, s);
+                const int qb = ui & 1;
+                ptx::mbar_wait(BAR(QFULL + qb), (ui >> 1) & 1u);
+                const uint32_t qbase = qsm + (uint32_t)qb * 4096;
+                for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {          // S^T = K_tile . Q^T
+                    const int st = it % ST;
+                    ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                    const int sb = si & 1;
+                    ptx::mbar_wait(BAR(SFREE + sb), ((si >> 1) & 1u) ^ 1u);
+                    ptx::tc_fence_after();
+                    const uint32_t base = ring + (uint32_t)st * kStageBytes;
 #pragma unroll
-            for (int g = 0; g < GP; ++g) red[64 + q4 * 16 + g] = z[g];
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t da = ptx::smem_desc_sw128(base + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
+                        const uint64_t db = ptx::smem_desc_sw128(qbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+                        ptx::mma_bf16(tmem + (uint32_t)sb * 16, da, db, idesc_qk, kk > 0);
+                    }
+                    ptx::mma_commit(BAR(SFULL + sb));
+                    ptx::mma_commit(BAR(EMPTY + st));
+                }
+                ptx::mma_commit(BAR(QFREE + qb));
+                ptx::mbar_wait(BAR(OFREE), (ui & 1u) ^ 1u);               // previous O drained
+                for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
+                    const int st = it % ST;
+                    ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                    const int pb = pi & 1;
+                    ptx::mbar_wait(BAR(PREADY + pb), (pi >> 1) & 1u);
+                    ptx::tc_fence_after();
+                    const uint32_t base = ring + (uint32_t)st * kStageBytes;
+                    const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const uint64_t da = ptx::smem_desc_sw128(base + kk * 2048, kBoxBytes, 1024);
+                        const uint64_t db = ptx::smem_desc_sw128(pbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
+                        ptx::mma_bf16(tmem + 32, da, db, idesc_pv, (t | kk) > 0);
+                    }
+                    ptx::mma_commit(BAR(EMPTY + st));
+                    ptx::mma_commit(BAR(PFREE + pb));
+                }
+                ptx::mma_commit(BAR(OFULL));
+            }
         }
-        ptx::named_bar_sync(1, 128);
-        if (tid == 64) {
-            for (int g = 0; g < G; ++g)
-                ex_z[g] = ((red[64 + 0 * 16 + g] + red[64 + 1 * 16 + g]) + red[64 + 2 * 16 + g]) + red[64 + 3 * 16 + g];
-        }
-        // un-normalised O^T from TMEM: this thread's lane is d = row
-        ptx::mbar_wait(BAR(OFULL), 0);
-        ptx::tc_fence_after();
-        if (ntiles > 0) {
-            uint32_t o[16];
-            ptx::tmem_ld_x16(tl + 32, o);
-            ptx::tmem_ld_wait();
+        __syncwarp();
+    } else {
+        // ------------------------------ softmax / score / exchange warps -------------------------
+        const int q4 = warp & 3;
+        const int sidx = tid - 64;
+        const int row = 32 * q4 + lane;               // token row of a tile / d index of O
+        const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
+        float* xs = misc;          // [16] x_g* (current token)
+        float* gM = misc + 16;     // [16]
+        float* glz = misc + 32;    // [16]
+        float* gZ = misc + 48;     // [16]
+        int* s_slot = (int*)(misc + 64);
+        unsigned long long* kred = (unsigned long long*)(red + 128);
+        const int box = row >> 6, cc = row & 63;
+        const float log2G = log2f((float)G);
+        const float invG = 1.0f / (float)G;
+        uint32_t it = 0, si = 0, pi = 0, ui = 0;
+        for (int u = cid; u < units; u += C, ++ui) {
+            const UnitInfo x = unit_info(p, u, s);
+            const int nv = x.nv;
+            // current token's logit x_g* (P:50-51): warp w-2 takes heads g = w-2, w+2
+            for (int g = warp - 2; g < G; g += 4) {
+                const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
+                const uint16_t* kn = p.k_new + (size_t)u * 128;
+                float acc = 0.f;
+#pragma unroll
+                for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                if (lane == 0) xs[g] = acc * p.scale_log2;
+            }
+            // ---- K pass: logits to SMEM, running max
+            float mloc[GP];
+#pragma unroll
+            for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
+            for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {
+                const int st = it % ST, sb = si & 1;
+                ptx::mbar_wait(BAR(SFULL + sb), (si >> 1) & 1u);
+                ptx::tc_fence_after();
+                uint32_t r[8];
+                ptx::tmem_ld_x8(tl + (uint32_t)sb * 16, r);
+                ptx::tmem_ld_wait();
+                const int tok = t * 128 + row;
+                const bool valid = tok < nv;
+#pragma unroll
+                for (int g = 0; g < GP; ++g) {
+                    if (g < G) {
+                        const float xv = valid ? __uint_as_float(r[g]) * p.scale_log2 : -INFINITY;
+                        X[g * chunk + tok] = xv;
+                        mloc[g] = fmaxf(mloc[g], xv);
+                    }
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(BAR(SFREE + sb));
+                    ptx::mbar_arrive(BAR(EMPTY + st));
+                }
+            }
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) mloc[g] = fmaxf(mloc[g], __shfl_xor_sync(0xffffffffu, mloc[g], off));
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int g = 0; g < GP; ++g) red[q4 * 16 + g] = mloc[g];
+            }
+            ptx::named_bar_sync(1, 128);
+            float m[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g)
-                if (g < G) ex_o[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
-        } else {
-            for (int g = 0; g < G; ++g) ex_o[g * 128 + row] = 0.f;
+                m[g] = fmaxf(fmaxf(red[0 * 16 + g], red[1 * 16 + g]), fmaxf(red[2 * 16 + g], red[3 * 16 + g]));
+            // ---- V pass: P (hi/lo bf16) for the MMA, Z, lambda
+            float z[GP];
+#pragma unroll
+            for (int g = 0; g < GP; ++g) z[g] = 0.f;
+            for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {
+                const int pb = pi & 1;
+                ptx::mbar_wait(BAR(PFREE + pb), ((pi >> 1) & 1u) ^ 1u);
+                const int tok = t * 128 + row;
+                const bool valid = tok < nv;
+                unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
+#pragma unroll
+                for (int g = 0; g < GP; ++g) {
+                    if (g < G) {
+                        const float pv = valid ? exp2f(X[g * chunk + tok] - m[g]) : 0.f;
+                        z[g] += pv;
+                        const uint16_t hi = f32_to_bf16_rne(pv);
+                        const uint16_t lo = f32_to_bf16_rne(pv - bf16_to_f32(hi));
+                        *(uint16_t*)(P + g * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = hi;
+                        *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
+                    }
+                }
+                const int st = it % ST;
+                ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);      // V tile landed
+                unsigned char* Vt = smem + so.ring + st * kStageBytes;
+                if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
+#pragma unroll
+                    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            *(uint4*)(Vt + bb * kBoxBytes + row * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
+                float lam = 0.f;
+                if (valid) {
+#pragma unroll
+                    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                        for (int c = 0; c < 8; ++c)
+                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((c ^ (row & 7)) << 4)));
+                }
+                Ls[tok] = lam;
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(BAR(EMPTY + st));
+            }
+#pragma unroll
+            for (int g = 0; g < GP; ++g) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) z[g] += __shfl_xor_sync(0xffffffffu, z[g], off);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int g = 0; g < GP; ++g) red[64 + q4 * 16 + g] = z[g];
+            }
+            // ---- publish (m, Z, o) in this unit's exchange buffer
+            const int xp = ui & 1;
+            const uint32_t use = ui >> 1;
+            Xchg* xc = xb + xp;
+            ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // readers of its last use are done
+            ptx::mbar_wait(BAR(OFULL), ui & 1u);
+            ptx::tc_fence_after();
+            if (x.ntiles > 0) {
+                uint32_t o[16];
+                ptx::tmem_ld_x16(tl + 32, o);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int g = 0; g < GP; ++g)
+                    if (g < G) xc->o[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
+            } else {
+                for (int g = 0; g < G; ++g) xc->o[g * 128 + row] = 0.f;
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
+            ptx::named_bar_sync(1, 128);                                // red[] and xc->o complete
+            if (sidx < G) {
+                const int g = sidx;
+                xc->m[g] = fmaxf(fmaxf(red[0 * 16 + g], red[1 * 16 + g]), fmaxf(red[2 * 16 + g], red[3 * 16 + g]));
+                xc->z[g] = ((red[64 + 0 * 16 + g] + red[64 + 1 * 16 + g]) + red[64 + 2 * 16 + g]) + red[64 + 3 * 16 + g];
+            }
+            ptx::named_bar_sync(1, 128);
+            const uint32_t xr_local = BAR(XREADY + xp);
+            if (sidx == 0) {
+                ptx::fence_acq_rel_cluster();
+                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(xr_local, r));
+            }
+            ptx::mbar_wait_cluster(xr_local, use & 1u);
+            // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
+            const uint32_t xc_addr = ptx::smem_u32(xc);
+            if (sidx < G) {
+                const int g = sidx;
+                float M = xs[g];
+                for (int r = 0; r < S; ++r)
+                    M = fmaxf(M, ptx::ld_dsmem_f32(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, m) + 4 * g, r)));
+                float Z = 0.f;
+                for (int r = 0; r < S; ++r) {
+                    const uint32_t ra = ptx::mapa(xc_addr, r);
+                    const float mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
+                    const float zr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, z) + 4 * g);
+                    Z += zr * exp2f(mr - M);
+                }
+                Z += exp2f(xs[g] - M);
+                gM[g] = M;
+                gZ[g] = Z;
+                glz[g] = log2f(Z);
+            }
+            ptx::named_bar_sync(1, 128);
+            if (s != 0 && sidx == 0) {   // done reading every rank's (m, Z): release them
+                ptx::fence_acq_rel_cluster();
+                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
+            }
+            // ---- scores I_j (Eq. 6, mean over the group) and the local argmin key
+            unsigned long long best = ~0ull;
+            float wM[GP];
+#pragma unroll
+            for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
+            for (int j = sidx; j < nv; j += 128) {
+                const float lam = Ls[j];
+                float av[GP];
+                float amax = -INFINITY;
+#pragma unroll
+                for (int g = 0; g < GP; ++g) {
+                    av[g] = g < G ? X[g * chunk + j] - wM[g] : -INFINITY;
+                    amax = fmaxf(amax, av[g]);
+                }
+                float ssum = 0.f;
+#pragma unroll
+                for (int g = 0; g < GP; ++g) ssum += exp2f(av[g] - amax);
+                const float ls = log2f(lam) + amax + log2f(ssum) - log2G;   // log2 I_j, no underflow
+                if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * exp2f(amax) * ssum * invG;
+                best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
+            }
+            if (p.scores)
+                for (int j = nv + sidx; j < x.c1 - x.c0; j += 128) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
+            if (lane == 0) kred[q4] = best;
+            ptx::named_bar_sync(1, 128);
+            if (sidx == 0) {
+                xc->key = umin64(umin64(kred[0], kred[1]), umin64(kred[2], kred[3]));
+                ptx::fence_acq_rel_cluster();
+                ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
+            }
+            if (s == 0) {
+                // ---- rank 0: slot, output combine, in-place eviction write
+                ptx::mbar_wait_cluster(BAR(KREADY + xp), use & 1u);
+                if (sidx == 0) {
+                    unsigned long long mk = ~0ull;
+                    for (int r = 0; r < S; ++r)
+                        mk = umin64(mk, ptx::ld_dsmem_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key), r)));
+                    const int sl = x.n < N ? x.n : (int)(mk & 0xffffffffull);
+                    *s_slot = sl;
+                    p.slot[u] = sl;
+                    if (x.n < N) p.n_valid[u] = x.n + 1;
+                }
+                ptx::named_bar_sync(1, 128);
+                const int sl = *s_slot;
+                const uint16_t* vn = p.v_new + (size_t)u * 128;
+                for (int i = sidx; i < G * 128; i += 128) {
+                    const int g = i >> 7, l = i & 127;
+                    float acc = 0.f;
+                    for (int r = 0; r < S; ++r) {
+                        const uint32_t ra = ptx::mapa(xc_addr, r);
+                        const float mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
+                        acc += ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, o) + 4 * i) * exp2f(mr - gM[g]);
+                    }
+                    acc += exp2f(xs[g] - gM[g]) * bf16_to_f32(vn[l]);
+                    const float ov = acc / gZ[g];
+                    const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
+                    if (p.out_f32) ((float*)p.out)[oi] = ov;
+                    else ((uint16_t*)p.out)[oi] = f32_to_bf16_rne(ov);
+                }
+                // every CTA of the cluster consumed unit u's K/V before arriving on kready
+                if (sidx < 16) {
+                    const size_t unit_off = (size_t)u * N * 128;
+                    const uint4* ks = (const uint4*)(p.k_new + (size_t)u * 128);
+                    const uint4* vs = (const uint4*)(p.v_new + (size_t)u * 128);
+                    ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = ks[sidx];
+                    ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = vs[sidx];
+                }
+                ptx::named_bar_sync(1, 128);
+                if (sidx == 0) {
+                    ptx::fence_acq_rel_cluster();
+                    for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
+                }
+            }
         }
-        ptx::tc_fence_before();
+        // drain: no CTA leaves while a peer may still read its exchange buffers
+        for (uint32_t k = ui >= 2 ? ui - 2 : 0; k < ui; ++k)
+            ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
     }
     __syncthreads();
-    Partials pt{ex_m, ex_z, ex_o, X, Ls, misc, keys};
-    cluster_finalize<128, GP, kNT>(p, pt, u, n, c0, c1, nv);
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<kTmemCols>(tmem);
     }
 }
 
+__host__ __device__ constexpr int gpad_tc(int G) { return G <= 4 ? 4 : 8; }
+
 template <int GP>
-cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) {
-    auto kern = tc_decode_kernel<GP>;
+cudaError_t set_attrs(int smem, int splits) {
     static int smem_set[64] = {0};
     static bool np_set[64] = {false};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (dev < 64 && plan.smem > smem_set[dev]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
+    if (dev >= 64 || smem > smem_set[dev]) {
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        smem_set[dev] = plan.smem;
+        if (dev < 64) smem_set[dev] = smem;
     }
-    if (plan.splits > 8 && dev < 64 && !np_set[dev]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (splits > 8 && (dev >= 64 || !np_set[dev])) {
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        np_set[dev] = true;
+        if (dev < 64) np_set[dev] = true;
+    }
+    return cudaSuccess;
+}
+
+template <int GP>
+int max_active_clusters(int splits, int smem) {
+    if (set_attrs<GP>(smem, splits) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(plan.splits * args.p.B * args.p.Hkv, 1, 1);
+    cfg.gridDim = dim3(splits * 1024, 1, 1);
+    cfg.blockDim = dim3(kNT, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = splits;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+template <int GP>
+cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) {
+    cudaError_t e = set_attrs<GP>(plan.smem, plan.splits);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(plan.splits * args.clusters, 1, 1);
     cfg.blockDim = dim3(kNT, 1, 1);
     cfg.dynamicSmemBytes = plan.smem;
     cfg.stream = stream;
@@ -367,10 +582,8 @@ cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, args);
+    return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP>, args);
 }
-
-__host__ __device__ constexpr int gpad_tc(int G) { return G <= 4 ? 4 : 8; }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -397,35 +610,56 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t rows, int d) {
     return r == CUDA_SUCCESS;
 }
 
+int stages_for(int G, int chunk) {
+    const int base = tc_smem(G, chunk, 0).total;
+    int st = (kSmemLimit - base) / kStageBytes;
+    return st > kMaxStages ? kMaxStages : st;
+}
+
 }  // namespace
 
 bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 
+// Split plan: for each cluster size S in {1, 2, 4, 8, 16} whose chunk leaves room for >= 3 ring
+// stages beside X and lambda, the persistent grid holds C_S = cudaOccupancyMaxActiveClusters
+// clusters (capped at the unit count) and needs ceil(units / C_S) rounds of `chunk` tokens per
+// CTA; the plan minimises rounds * (chunk + 256)  (256 tokens ~ the per-unit exchange overhead).
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
-    Plan pl;
-    pl.kernel = LF_KERNEL_TCGEN05;
-    const int GP = gpad_tc(G);
-    const int fixed = tc_smem(G, GP, 0).total;
-    int chunk_max = (kMaxSmem - fixed) / ((G + 1) * 4) / 128 * 128;
-    if (chunk_max < 128) chunk_max = 128;
-    const int Nr = (N + 127) / 128 * 128;
-    int chunk;
-    if (split_tokens > 0) {
-        chunk = split_tokens;
-    } else {
-        int want = (2 * num_sms + units - 1) / units;        // >= one wave of 2 CTAs per SM
-        int smin = (Nr + chunk_max - 1) / chunk_max;
-        int S = want > smin ? want : smin;
-        int cap = smin > 8 ? 16 : 8;
-        if (S > cap) S = cap;
-        chunk = ((Nr + S - 1) / S + 127) / 128 * 128;
-    }
-    pl.chunk = chunk;
-    pl.splits = (N + chunk - 1) / chunk;
-    pl.smem = tc_smem(G, GP, chunk).total;
-    if (pl.smem > 227 * 1024) pl.splits = -1;
     (void)d;
-    return pl;
+    (void)num_sms;
+    Plan best;
+    best.kernel = LF_KERNEL_TCGEN05;
+    best.splits = -1;
+    best.chunk = 0;
+    best.smem = 0;
+    best.clusters = 0;
+    best.stages = 0;
+    const int Nr = (N + 127) / 128 * 128;
+    long long best_cost = -1;
+    for (int S = 1; S <= 16; S *= 2) {
+        const int chunk = split_tokens > 0 ? split_tokens : ((Nr + S - 1) / S + 127) / 128 * 128;
+        const int splits = (N + chunk - 1) / chunk;
+        if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
+        if (splits > 16) continue;
+        const int st = stages_for(G, chunk);
+        if (st < 3) continue;
+        const int smem = tc_smem(G, chunk, st).total;
+        const int C = gpad_tc(G) == 4 ? max_active_clusters<4>(splits, smem) : max_active_clusters<8>(splits, smem);
+        if (C <= 0) continue;
+        const int Cu = C < units ? C : units;
+        const long long rounds = (units + Cu - 1) / Cu;
+        const long long cost = rounds * (chunk + 256);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best.splits = splits;
+            best.chunk = chunk;
+            best.smem = smem;
+            best.clusters = Cu;
+            best.stages = st;
+        }
+        if (split_tokens > 0) break;
+    }
+    return best;
 }
 
 bool tc_make_maps(TcMaps* maps, void* K, void* V, long long units, int N, int d) {
@@ -439,6 +673,8 @@ cudaError_t tc_launch(const StepParams& p, const Plan& plan, const TcMaps& maps,
     memcpy(&args.tmK, maps.k, sizeof(CUtensorMap));
     memcpy(&args.tmV, maps.v, sizeof(CUtensorMap));
     args.p = p;
+    args.clusters = plan.clusters;
+    args.stages = plan.stages;
     if (gpad_tc(p.G) == 4) return launch_t<4>(args, plan, stream);
     return launch_t<8>(args, plan, stream);
 }

@@ -30,6 +30,8 @@ struct Plan {
     int32_t splits;
     int32_t chunk;
     int32_t smem;     // dynamic shared memory bytes per CTA
+    int32_t clusters; // persistent clusters in the grid (tcgen05 kernel), 0 = one cluster per unit
+    int32_t stages;   // TMA ring depth (tcgen05 kernel)
 };
 
 // CUDA-core split-KV kernel (lf_decode_simt.cu)

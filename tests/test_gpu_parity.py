@@ -58,6 +58,8 @@ SHAPES = [  # (B, Hq, Hkv, d, N, prefill, steps, split_tokens)
     (1, 8, 1, 64, 1000, 995, 12, 256),  # G=8, d=64, 4 splits
     (4, 32, 8, 128, 512, 500, 16, 0),   # Q3-like group structure
     (1, 2, 1, 128, 700, 650, 60, 0),    # G=2 crossing the fill boundary
+    (64, 32, 8, 128, 384, 380, 6, 0),   # 512 units: several units per persistent cluster
+    (48, 32, 8, 128, 384, 370, 14, 128),  # 384 units x 3-CTA clusters, fill -> evict
 ]
 
 
