@@ -2,11 +2,13 @@
 //
 // Grid = C persistent clusters of S CTAs (1 CTA per SM).  Cluster c handles units
 // u = c, c + C, c + 2C, ... (unit = (sequence, kv head)); CTA s of the cluster owns slots
-// [s*chunk, (s+1)*chunk) of every unit.  Warp roles (192 threads):
+// [s*chunk, (s+1)*chunk) of every unit.  Warp roles (320 threads):
 //   warp 0     producer: Q rows of the next unit (LDG -> swizzled SMEM) and the K then V tiles
 //              (128 tokens x 128 d, two SWIZZLE_128B TMA boxes) through an ST-stage ring
 //   warp 1     TMEM allocator + tcgen05.mma issuer (one lane)
-//   warps 2-5  softmax / score / exchange warps; warp w owns TMEM lanes [32(w%4), 32(w%4)+32)
+//   warps 2-9  softmax / score / exchange warps in two groups of four that take alternate tiles
+//              (S and P buffers are double buffered by tile parity); warp w owns TMEM lanes
+//              [32(w%4), 32(w%4)+32)
 // The producer and MMA warps run ahead into the next unit while the softmax warps finish the
 // current one, so the HBM stream does not drain at unit boundaries.
 //
@@ -31,7 +33,7 @@
 namespace lf {
 namespace {
 
-constexpr int kNT = 192;
+constexpr int kNT = 320;      // producer, MMA, 2 x 4 softmax warps
 constexpr int kStageBytes = 32768;   // 128 tokens x 128 d x bf16 (two 16 KB boxes)
 constexpr int kBoxBytes = 16384;
 constexpr int kSmemLimit = 227 * 1024;
@@ -68,7 +70,7 @@ __host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 128 * 4;
-    s.red = off;  off += 3 * 4 * 16 * 4;
+    s.red = off;  off += 320 * 4;
     s.bars = off; off += 40 * 8;
     s.tmem = off; off += 16;
     s.total = off + 1024;                        // slack for 1024-byte alignment of the base
@@ -158,7 +160,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     if (warp == 1) ptx::tmem_alloc<kTmemCols>(ptx::smem_u32(smem + so.tmem));
     if (warp >= 2) {   // zero both Q and both P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
-        for (int e = tid - 64; e < 4 * 4096 / 16; e += 128) z[e] = make_uint4(0, 0, 0, 0);
+        for (int e = tid - 64; e < 4 * 4096 / 16; e += 256) z[e] = make_uint4(0, 0, 0, 0);
         ptx::fence_proxy_async_smem();
     }
     ptx::tc_fence_before();
@@ -250,8 +252,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         __syncwarp();
     } else {
         // ------------------------------ softmax / score / exchange warps -------------------------
+        const int grp = (warp - 2) >> 2;              // two groups take alternate tiles
         const int q4 = warp & 3;
-        const int sidx = tid - 64;
+        const int sidx = tid - 64;                    // 0..255
         const int row = 32 * q4 + lane;               // token row of a tile / d index of O
         const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
         float* xs = misc;          // [16] x_g* (current token)
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         float* glz = misc + 32;    // [16]
         float* gZ = misc + 48;     // [16]
         int* s_slot = (int*)(misc + 64);
-        unsigned long long* kred = (unsigned long long*)(red + 128);
+        unsigned long long* kred = (unsigned long long*)(red + 256);
         const int box = row >> 6, cc = row & 63;
         const float log2G = log2f((float)G);
         const float invG = 1.0f / (float)G;
@@ -267,8 +270,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         for (int u = cid; u < units; u += C, ++ui) {
             const UnitInfo x = unit_info(p, u, s);
             const int nv = x.nv;
-            // current token's logit x_g* (P:50-51): warp w-2 takes heads g = w-2, w+2
-            for (int g = warp - 2; g < G; g += 4) {
+            // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
+            for (int g = warp - 2; g < G; g += 8) {
                 const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
                 const uint16_t* kn = p.k_new + (size_t)u * 128;
                 float acc = 0.f;
@@ -282,9 +285,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             float mloc[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
-            for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {
-                const int st = it % ST, sb = si & 1;
-                ptx::mbar_wait(BAR(SFULL + sb), (si >> 1) & 1u);
+            for (int t = 0; t < x.ntiles; ++t) {
+                const uint32_t c = si + t;
+                if ((int)(c & 1u) != grp) continue;
+                const int st = (it + t) % ST, sb = c & 1;
+                ptx::mbar_wait(BAR(SFULL + sb), (c >> 1) & 1u);
                 ptx::tc_fence_after();
                 uint32_t r[8];
                 ptx::tmem_ld_x8(tl + (uint32_t)sb * 16, r);
@@ -306,6 +311,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     ptx::mbar_arrive(BAR(EMPTY + st));
                 }
             }
+            si += x.ntiles;
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
 #pragma unroll
@@ -313,20 +319,25 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             }
             if (lane == 0) {
 #pragma unroll
-                for (int g = 0; g < GP; ++g) red[q4 * 16 + g] = mloc[g];
+                for (int g = 0; g < GP; ++g) red[(grp * 4 + q4) * 16 + g] = mloc[g];
             }
-            ptx::named_bar_sync(1, 128);
+            ptx::named_bar_sync(1, 256);
             float m[GP];
 #pragma unroll
-            for (int g = 0; g < GP; ++g)
-                m[g] = fmaxf(fmaxf(red[0 * 16 + g], red[1 * 16 + g]), fmaxf(red[2 * 16 + g], red[3 * 16 + g]));
+            for (int g = 0; g < GP; ++g) {
+                m[g] = red[g];
+#pragma unroll
+                for (int w = 1; w < 8; ++w) m[g] = fmaxf(m[g], red[w * 16 + g]);
+            }
             // ---- V pass: P (hi/lo bf16) for the MMA, Z, lambda
             float z[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) z[g] = 0.f;
-            for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {
-                const int pb = pi & 1;
-                ptx::mbar_wait(BAR(PFREE + pb), ((pi >> 1) & 1u) ^ 1u);
+            for (int t = 0; t < x.ntiles; ++t) {
+                const uint32_t c = pi + t;
+                if ((int)(c & 1u) != grp) continue;
+                const int pb = c & 1;
+                ptx::mbar_wait(BAR(PFREE + pb), ((c >> 1) & 1u) ^ 1u);
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
                 unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
@@ -341,8 +352,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                         *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
                     }
                 }
-                const int st = it % ST;
-                ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);      // V tile landed
+                const uint32_t iv = it + x.ntiles + t;
+                const int st = iv % ST;
+                ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
 #pragma unroll
@@ -366,6 +378,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(EMPTY + st));
             }
+            pi += x.ntiles;
+            it += 2 * x.ntiles;
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
 #pragma unroll
@@ -373,35 +387,42 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             }
             if (lane == 0) {
 #pragma unroll
-                for (int g = 0; g < GP; ++g) red[64 + q4 * 16 + g] = z[g];
+                for (int g = 0; g < GP; ++g) red[128 + (grp * 4 + q4) * 16 + g] = z[g];
             }
             // ---- publish (m, Z, o) in this unit's exchange buffer
             const int xp = ui & 1;
             const uint32_t use = ui >> 1;
             Xchg* xc = xb + xp;
             ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // readers of its last use are done
-            ptx::mbar_wait(BAR(OFULL), ui & 1u);
-            ptx::tc_fence_after();
-            if (x.ntiles > 0) {
-                uint32_t o[16];
-                ptx::tmem_ld_x16(tl + 32, o);
-                ptx::tmem_ld_wait();
+            if (grp == 0) {   // group 0 drains O (TMEM lane = d)
+                ptx::mbar_wait(BAR(OFULL), ui & 1u);
+                ptx::tc_fence_after();
+                if (x.ntiles > 0) {
+                    uint32_t o[16];
+                    ptx::tmem_ld_x16(tl + 32, o);
+                    ptx::tmem_ld_wait();
 #pragma unroll
-                for (int g = 0; g < GP; ++g)
-                    if (g < G) xc->o[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
-            } else {
-                for (int g = 0; g < G; ++g) xc->o[g * 128 + row] = 0.f;
+                    for (int g = 0; g < GP; ++g)
+                        if (g < G) xc->o[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
+                } else {
+                    for (int g = 0; g < G; ++g) xc->o[g * 128 + row] = 0.f;
+                }
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
-            ptx::named_bar_sync(1, 128);                                // red[] and xc->o complete
+            ptx::named_bar_sync(1, 256);                                // red[] and xc->o complete
             if (sidx < G) {
                 const int g = sidx;
-                xc->m[g] = fmaxf(fmaxf(red[0 * 16 + g], red[1 * 16 + g]), fmaxf(red[2 * 16 + g], red[3 * 16 + g]));
-                xc->z[g] = ((red[64 + 0 * 16 + g] + red[64 + 1 * 16 + g]) + red[64 + 2 * 16 + g]) + red[64 + 3 * 16 + g];
+                float mm = red[g], zz = red[128 + g];
+                for (int w = 1; w < 8; ++w) {
+                    mm = fmaxf(mm, red[w * 16 + g]);
+                    zz += red[128 + w * 16 + g];
+                }
+                xc->m[g] = mm;
+                xc->z[g] = zz;
             }
-            ptx::named_bar_sync(1, 128);
+            ptx::named_bar_sync(1, 256);
             const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) {
                 ptx::fence_acq_rel_cluster();
@@ -427,7 +448,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 gZ[g] = Z;
                 glz[g] = log2f(Z);
             }
-            ptx::named_bar_sync(1, 128);
+            ptx::named_bar_sync(1, 256);
             if (s != 0 && sidx == 0) {   // done reading every rank's (m, Z): release them
                 ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
@@ -437,7 +458,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             float wM[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
-            for (int j = sidx; j < nv; j += 128) {
+            for (int j = sidx; j < nv; j += 256) {
                 const float lam = Ls[j];
                 float av[GP];
                 float amax = -INFINITY;
@@ -454,13 +475,15 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
             }
             if (p.scores)
-                for (int j = nv + sidx; j < x.c1 - x.c0; j += 128) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
+                for (int j = nv + sidx; j < x.c1 - x.c0; j += 256) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
-            if (lane == 0) kred[q4] = best;
-            ptx::named_bar_sync(1, 128);
+            if (lane == 0) kred[warp - 2] = best;
+            ptx::named_bar_sync(1, 256);
             if (sidx == 0) {
-                xc->key = umin64(umin64(kred[0], kred[1]), umin64(kred[2], kred[3]));
+                unsigned long long kb = kred[0];
+                for (int w = 1; w < 8; ++w) kb = umin64(kb, kred[w]);
+                xc->key = kb;
                 ptx::fence_acq_rel_cluster();
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
             }
@@ -476,10 +499,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     p.slot[u] = sl;
                     if (x.n < N) p.n_valid[u] = x.n + 1;
                 }
-                ptx::named_bar_sync(1, 128);
+                ptx::named_bar_sync(1, 256);
                 const int sl = *s_slot;
                 const uint16_t* vn = p.v_new + (size_t)u * 128;
-                for (int i = sidx; i < G * 128; i += 128) {
+                for (int i = sidx; i < G * 128; i += 256) {
                     const int g = i >> 7, l = i & 127;
                     float acc = 0.f;
                     for (int r = 0; r < S; ++r) {
@@ -501,7 +524,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = ks[sidx];
                     ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = vs[sidx];
                 }
-                ptx::named_bar_sync(1, 128);
+                ptx::named_bar_sync(1, 256);
                 if (sidx == 0) {
                     ptx::fence_acq_rel_cluster();
                     for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
