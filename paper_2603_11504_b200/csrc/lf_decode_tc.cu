@@ -33,12 +33,15 @@
 namespace lf {
 namespace {
 
-constexpr int kNT = 320;      // producer, MMA, 2 x 4 softmax warps
+constexpr int kNG = 3;                  // softmax warp groups (4 warps each), alternate tiles
+constexpr int kNT = 64 + 128 * kNG;     // + producer warp + MMA warp
+constexpr int kNS = 128 * kNG;          // softmax threads
 constexpr int kStageBytes = 32768;   // 128 tokens x 128 d x bf16 (two 16 KB boxes)
 constexpr int kBoxBytes = 16384;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxStages = 6;
-constexpr uint32_t kTmemCols = 64;   // S double buffer (2 x 16) + O (16), power of two
+constexpr uint32_t kTmemCols = (kNG * 16 + 16) <= 64 ? 64 : 128;   // S per group (16 each) + O (16)
+constexpr uint32_t kOCol = kNG * 16;
 
 struct TcArgs {
     CUtensorMap tmK;
@@ -65,12 +68,12 @@ __host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
     int off = 0;
     s.ring = off; off += stages * kStageBytes;   // 1024-aligned (swizzle atoms)
     s.q = off;    off += 2 * 4096;               // Q^T operand x2 (per unit parity): 16 rows x 128 d
-    s.pbuf = off; off += 2 * 4096;               // P^T operand x2: 16 rows x 128 tokens
+    s.pbuf = off; off += kNG * 4096;             // P^T operand per group: 16 rows x 128 tokens
     s.X = off;    off += G * chunk * 4;          // x_gj of the current unit
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 128 * 4;
-    s.red = off;  off += 320 * 4;
+    s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
     s.bars = off; off += 40 * 8;
     s.tmem = off; off += 16;
     s.total = off + 1024;                        // slack for 1024-byte alignment of the base
@@ -80,8 +83,8 @@ __host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
 // mbarrier slots
 constexpr int FULL = 0;                 // [kMaxStages]
 constexpr int EMPTY = FULL + kMaxStages;
-constexpr int SFULL = EMPTY + kMaxStages, SFREE = SFULL + 2, PREADY = SFREE + 2, PFREE = PREADY + 2;
-constexpr int QFULL = PFREE + 2, QFREE = QFULL + 2, OFULL = QFREE + 2, OFREE = OFULL + 1;
+constexpr int SFULL = EMPTY + kMaxStages, SFREE = SFULL + kNG, PREADY = SFREE + kNG, PFREE = PREADY + kNG;
+constexpr int QFULL = PFREE + kNG, QFREE = QFULL + 2, OFULL = QFREE + 2, OFREE = OFULL + 1;
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 40, "barrier slots");
 
@@ -140,11 +143,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             ptx::mbar_init(BAR(FULL + i), 1);      // producer's expect_tx arrival
             ptx::mbar_init(BAR(EMPTY + i), 5);     // MMA commit + 4 softmax warps
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kNG; ++i) {
             ptx::mbar_init(BAR(SFULL + i), 1);
             ptx::mbar_init(BAR(SFREE + i), 4);
             ptx::mbar_init(BAR(PREADY + i), 4);
             ptx::mbar_init(BAR(PFREE + i), 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(BAR(QFULL + i), 1);
             ptx::mbar_init(BAR(QFREE + i), 1);
             ptx::mbar_init(BAR(XREADY + i), S);    // one arrival per rank
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     if (warp == 1) ptx::tmem_alloc<kTmemCols>(ptx::smem_u32(smem + so.tmem));
     if (warp >= 2) {   // zero both Q and both P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
-        for (int e = tid - 64; e < 4 * 4096 / 16; e += 256) z[e] = make_uint4(0, 0, 0, 0);
+        for (int e = tid - 64; e < (2 + kNG) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
         ptx::fence_proxy_async_smem();
     }
     ptx::tc_fence_before();
@@ -214,8 +219,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {          // S^T = K_tile . Q^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    const int sb = si & 1;
-                    ptx::mbar_wait(BAR(SFREE + sb), ((si >> 1) & 1u) ^ 1u);
+                    const int sb = si % kNG;
+                    ptx::mbar_wait(BAR(SFREE + sb), ((si / kNG) & 1u) ^ 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
 #pragma unroll
@@ -232,8 +237,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    const int pb = pi & 1;
-                    ptx::mbar_wait(BAR(PREADY + pb), (pi >> 1) & 1u);
+                    const int pb = pi % kNG;
+                    ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
@@ -241,7 +246,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     for (int kk = 0; kk < 8; ++kk) {
                         const uint64_t da = ptx::smem_desc_sw128(base + kk * 2048, kBoxBytes, 1024);
                         const uint64_t db = ptx::smem_desc_sw128(pbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                        ptx::mma_bf16(tmem + 32, da, db, idesc_pv, (t | kk) > 0);
+                        ptx::mma_bf16(tmem + kOCol, da, db, idesc_pv, (t | kk) > 0);
                     }
                     ptx::mma_commit(BAR(EMPTY + st));
                     ptx::mma_commit(BAR(PFREE + pb));
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         // ------------------------------ softmax / score / exchange warps -------------------------
         const int grp = (warp - 2) >> 2;              // two groups take alternate tiles
         const int q4 = warp & 3;
-        const int sidx = tid - 64;                    // 0..255
+        const int sidx = tid - 64;                    // 0 .. kNS-1
         const int row = 32 * q4 + lane;               // token row of a tile / d index of O
         const uint32_t tl = tmem + ((uint32_t)(32 * q4) << 16);
         float* xs = misc;          // [16] x_g* (current token)
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         float* glz = misc + 32;    // [16]
         float* gZ = misc + 48;     // [16]
         int* s_slot = (int*)(misc + 64);
-        unsigned long long* kred = (unsigned long long*)(red + 256);
+        unsigned long long* kred = (unsigned long long*)(red + 2 * kNG * 4 * 16);
         const int box = row >> 6, cc = row & 63;
         const float log2G = log2f((float)G);
         const float invG = 1.0f / (float)G;
@@ -271,7 +276,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             const UnitInfo x = unit_info(p, u, s);
             const int nv = x.nv;
             // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
-            for (int g = warp - 2; g < G; g += 8) {
+            for (int g = warp - 2; g < G; g += 4 * kNG) {
                 const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
                 const uint16_t* kn = p.k_new + (size_t)u * 128;
                 float acc = 0.f;
@@ -287,9 +292,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
             for (int t = 0; t < x.ntiles; ++t) {
                 const uint32_t c = si + t;
-                if ((int)(c & 1u) != grp) continue;
-                const int st = (it + t) % ST, sb = c & 1;
-                ptx::mbar_wait(BAR(SFULL + sb), (c >> 1) & 1u);
+                if ((int)(c % kNG) != grp) continue;
+                const int st = (it + t) % ST, sb = c % kNG;
+                ptx::mbar_wait(BAR(SFULL + sb), (c / kNG) & 1u);
                 ptx::tc_fence_after();
                 uint32_t r[8];
                 ptx::tmem_ld_x8(tl + (uint32_t)sb * 16, r);
@@ -321,13 +326,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
 #pragma unroll
                 for (int g = 0; g < GP; ++g) red[(grp * 4 + q4) * 16 + g] = mloc[g];
             }
-            ptx::named_bar_sync(1, 256);
+            ptx::named_bar_sync(1, kNS);
             float m[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
                 m[g] = red[g];
 #pragma unroll
-                for (int w = 1; w < 8; ++w) m[g] = fmaxf(m[g], red[w * 16 + g]);
+                for (int w = 1; w < 4 * kNG; ++w) m[g] = fmaxf(m[g], red[w * 16 + g]);
             }
             // ---- V pass: P (hi/lo bf16) for the MMA, Z, lambda
             float z[GP];
@@ -335,9 +340,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             for (int g = 0; g < GP; ++g) z[g] = 0.f;
             for (int t = 0; t < x.ntiles; ++t) {
                 const uint32_t c = pi + t;
-                if ((int)(c & 1u) != grp) continue;
-                const int pb = c & 1;
-                ptx::mbar_wait(BAR(PFREE + pb), ((c >> 1) & 1u) ^ 1u);
+                if ((int)(c % kNG) != grp) continue;
+                const int pb = c % kNG;
+                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNG) & 1u) ^ 1u);
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
                 unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             }
             if (lane == 0) {
 #pragma unroll
-                for (int g = 0; g < GP; ++g) red[128 + (grp * 4 + q4) * 16 + g] = z[g];
+                for (int g = 0; g < GP; ++g) red[kNG * 64 + (grp * 4 + q4) * 16 + g] = z[g];
             }
             // ---- publish (m, Z, o) in this unit's exchange buffer
             const int xp = ui & 1;
@@ -399,7 +404,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 ptx::tc_fence_after();
                 if (x.ntiles > 0) {
                     uint32_t o[16];
-                    ptx::tmem_ld_x16(tl + 32, o);
+                    ptx::tmem_ld_x16(tl + kOCol, o);
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int g = 0; g < GP; ++g)
@@ -411,18 +416,18 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
             }
-            ptx::named_bar_sync(1, 256);                                // red[] and xc->o complete
+            ptx::named_bar_sync(1, kNS);                                // red[] and xc->o complete
             if (sidx < G) {
                 const int g = sidx;
-                float mm = red[g], zz = red[128 + g];
-                for (int w = 1; w < 8; ++w) {
+                float mm = red[g], zz = red[kNG * 64 + g];
+                for (int w = 1; w < 4 * kNG; ++w) {
                     mm = fmaxf(mm, red[w * 16 + g]);
-                    zz += red[128 + w * 16 + g];
+                    zz += red[kNG * 64 + w * 16 + g];
                 }
                 xc->m[g] = mm;
                 xc->z[g] = zz;
             }
-            ptx::named_bar_sync(1, 256);
+            ptx::named_bar_sync(1, kNS);
             const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) {
                 ptx::fence_acq_rel_cluster();
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 gZ[g] = Z;
                 glz[g] = log2f(Z);
             }
-            ptx::named_bar_sync(1, 256);
+            ptx::named_bar_sync(1, kNS);
             if (s != 0 && sidx == 0) {   // done reading every rank's (m, Z): release them
                 ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             float wM[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
-            for (int j = sidx; j < nv; j += 256) {
+            for (int j = sidx; j < nv; j += kNS) {
                 const float lam = Ls[j];
                 float av[GP];
                 float amax = -INFINITY;
@@ -475,14 +480,14 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
             }
             if (p.scores)
-                for (int j = nv + sidx; j < x.c1 - x.c0; j += 256) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
+                for (int j = nv + sidx; j < x.c1 - x.c0; j += kNS) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
             if (lane == 0) kred[warp - 2] = best;
-            ptx::named_bar_sync(1, 256);
+            ptx::named_bar_sync(1, kNS);
             if (sidx == 0) {
                 unsigned long long kb = kred[0];
-                for (int w = 1; w < 8; ++w) kb = umin64(kb, kred[w]);
+                for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
                 xc->key = kb;
                 ptx::fence_acq_rel_cluster();
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
@@ -499,10 +504,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     p.slot[u] = sl;
                     if (x.n < N) p.n_valid[u] = x.n + 1;
                 }
-                ptx::named_bar_sync(1, 256);
+                ptx::named_bar_sync(1, kNS);
                 const int sl = *s_slot;
                 const uint16_t* vn = p.v_new + (size_t)u * 128;
-                for (int i = sidx; i < G * 128; i += 256) {
+                for (int i = sidx; i < G * 128; i += kNS) {
                     const int g = i >> 7, l = i & 127;
                     float acc = 0.f;
                     for (int r = 0; r < S; ++r) {
@@ -524,7 +529,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = ks[sidx];
                     ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = vs[sidx];
                 }
-                ptx::named_bar_sync(1, 256);
+                ptx::named_bar_sync(1, kNS);
                 if (sidx == 0) {
                     ptx::fence_acq_rel_cluster();
                     for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
