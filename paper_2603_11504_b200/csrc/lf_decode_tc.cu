@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
             ptx::mbar_init(BAR(FULL + i), 1);      // producer's expect_tx arrival
-            ptx::mbar_init(BAR(EMPTY + i), 5);     // MMA commit + 4 softmax warps
+            ptx::mbar_init(BAR(EMPTY + i), 1);     // MMA commit (the MMA is the stage's last reader)
         }
         for (int i = 0; i < kNG; ++i) {
             ptx::mbar_init(BAR(SFULL + i), 1);
@@ -311,10 +311,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(BAR(SFREE + sb));
-                    ptx::mbar_arrive(BAR(EMPTY + st));
-                }
+                if (lane == 0) ptx::mbar_arrive(BAR(SFREE + sb));
             }
             si += x.ntiles;
 #pragma unroll
@@ -368,9 +365,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                         for (int c = 0; c < 8; ++c)
                             *(uint4*)(Vt + bb * kBoxBytes + row * 128 + c * 16) = make_uint4(0, 0, 0, 0);
                 }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
+                // lambda_j from the landed tile, before PREADY: after the PV MMA the stage is refilled
                 float lam = 0.f;
                 if (valid) {
 #pragma unroll
@@ -380,8 +375,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                             lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((c ^ (row & 7)) << 4)));
                 }
                 Ls[tok] = lam;
+                ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(BAR(EMPTY + st));
+                if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
             }
             pi += x.ntiles;
             it += 2 * x.ntiles;
