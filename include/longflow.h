@@ -127,6 +127,10 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
 /* Number of CUDA kernels lf_decode_step launches per call (for launch accounting). */
 int32_t lf_kernels_per_step(const lf_cache* c);
 
+/* Debug only: device buffer receiving per-CTA %globaltimer events from builds compiled with
+ * -DLF_TRACE (ignored otherwise); NULL disables.  Layout: see DESIGN.md "Tracing". */
+lf_status lf_debug_set_trace(lf_cache* c, void* device_buf);
+
 const char* lf_status_string(lf_status s);
 const char* lf_last_error(void); /* thread-local detail text of the last failure */
 

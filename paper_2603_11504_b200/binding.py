@@ -24,7 +24,7 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 EXPORTS = ["lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
            "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_kernels_per_step",
-           "lf_status_string", "lf_last_error"]
+           "lf_debug_set_trace", "lf_status_string", "lf_last_error"]
 
 
 class LFError(RuntimeError):
@@ -43,7 +43,7 @@ class CacheConfig(ctypes.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
+def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     """Load liblongflow.so (raises if it has not been built: run __graft_entry__.build())."""
     global _lib
     if _lib is not None:
@@ -61,6 +61,8 @@ def load(path: str = LIB_PATH):
     lib.lf_decode_step_host.argtypes = [P, P, P, P, P, P, P]
     lib.lf_cache_views.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.lf_debug_set_trace.argtypes = [P, P]
+    lib.lf_debug_set_trace.restype = ctypes.c_int
     lib.lf_kernels_per_step.argtypes = [P]
     lib.lf_kernels_per_step.restype = i32
     for f in ("lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
@@ -186,6 +188,10 @@ class Cache:
         k, s, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _check(load().lf_cache_plan(self._h, ctypes.byref(k), ctypes.byref(s), ctypes.byref(c)), "plan")
         return dict(kernel=KERNEL_NAMES[k.value], splits=s.value, split_tokens=c.value)
+
+    def set_trace(self, buf):
+        """Debug: device buffer for the -DLF_TRACE event trace (None disables)."""
+        _check(load().lf_debug_set_trace(self._h, _ptr(buf)), "lf_debug_set_trace")
 
     def kernels_per_step(self) -> int:
         return int(load().lf_kernels_per_step(self._h))

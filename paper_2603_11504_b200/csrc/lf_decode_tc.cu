@@ -88,6 +88,22 @@ constexpr int QFULL = PFREE + kNG, QFREE = QFULL + 2, OFULL = QFREE + 2, OFREE =
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 40, "barrier slots");
 
+// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][8] u64.
+#ifdef LF_TRACE
+#define LF_EVENT(ui_, slot_)                                                                   \
+    do {                                                                                       \
+        if (p.trace) {                                                                         \
+            unsigned long long t_;                                                             \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 8 + (slot_)] = t_;              \
+        }                                                                                      \
+    } while (0)
+#else
+#define LF_EVENT(ui_, slot_) \
+    do {                     \
+    } while (0)
+#endif
+
 __device__ __forceinline__ float habs_sum8(const uint4& w) {
     return (fabsf(__uint_as_float(w.x << 16)) + fabsf(__uint_as_float(w.x & 0xffff0000u))) +
            (fabsf(__uint_as_float(w.y << 16)) + fabsf(__uint_as_float(w.y & 0xffff0000u))) +
@@ -190,6 +206,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             ptx::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
+                LF_EVENT(qi, 6);
                 ptx::mbar_arrive(BAR(QFULL + qb));
                 for (int i = 0; i < 2 * x.ntiles; ++i, ++it) {
                     const int st = it % ST;
@@ -215,6 +232,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 const UnitInfo x = unit_info(p, u, s);
                 const int qb = ui & 1;
                 ptx::mbar_wait(BAR(QFULL + qb), (ui >> 1) & 1u);
+                LF_EVENT(ui, 7);
                 const uint32_t qbase = qsm + (uint32_t)qb * 4096;
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {          // S^T = K_tile . Q^T
                     const int st = it % ST;
@@ -275,6 +293,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         for (int u = cid; u < units; u += C, ++ui) {
             const UnitInfo x = unit_info(p, u, s);
             const int nv = x.nv;
+            if (sidx == 0) LF_EVENT(ui, 0);
             // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
             for (int g = warp - 2; g < G; g += 4 * kNG) {
                 const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
@@ -324,6 +343,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int g = 0; g < GP; ++g) red[(grp * 4 + q4) * 16 + g] = mloc[g];
             }
             ptx::named_bar_sync(1, kNS);
+            if (sidx == 0) LF_EVENT(ui, 1);
             float m[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
@@ -390,6 +410,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
 #pragma unroll
                 for (int g = 0; g < GP; ++g) red[kNG * 64 + (grp * 4 + q4) * 16 + g] = z[g];
             }
+            if (sidx == 0) LF_EVENT(ui, 2);
             // ---- publish (m, Z, o) in this unit's exchange buffer
             const int xp = ui & 1;
             const uint32_t use = ui >> 1;
@@ -430,6 +451,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(xr_local, r));
             }
             ptx::mbar_wait_cluster(xr_local, use & 1u);
+            if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
             const uint32_t xc_addr = ptx::smem_u32(xc);
             if (sidx < G) {
@@ -482,6 +504,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             if (lane == 0) kred[warp - 2] = best;
             ptx::named_bar_sync(1, kNS);
             if (sidx == 0) {
+                LF_EVENT(ui, 4);
                 unsigned long long kb = kred[0];
                 for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
                 xc->key = kb;
@@ -533,6 +556,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             }
         }
         // drain: no CTA leaves while a peer may still read its exchange buffers
+        if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
         for (uint32_t k = ui >= 2 ? ui - 2 : 0; k < ui; ++k)
             ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
     }

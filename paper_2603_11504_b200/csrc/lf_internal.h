@@ -18,6 +18,7 @@ struct StepParams {
     void* out;              // bf16 or fp32 [B][Hq][d]
     int32_t* slot;          // int32 [B][Hkv]
     float* scores;          // fp32 [B][Hkv][N] or nullptr
+    unsigned long long* trace;  // debug event trace (LF_TRACE builds only), or nullptr
     int32_t B, Hq, Hkv, G, d, N;
     int32_t out_f32;        // 1: fp32 out, 0: bf16 out
     float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip

@@ -99,6 +99,7 @@ struct lf_cache {
     Layout L;
     lf::Plan plan;
     lf::TcMaps maps;
+    unsigned long long* trace;
 };
 
 namespace {
@@ -250,6 +251,12 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int
 
 int32_t lf_kernels_per_step(const lf_cache* c) { return c ? 1 : 0; }
 
+lf_status lf_debug_set_trace(lf_cache* c, void* device_buf) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    c->trace = (unsigned long long*)device_buf;
+    return LF_OK;
+}
+
 lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v, int32_t n,
                           void* stream) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
@@ -302,6 +309,7 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.out = out;
     p.slot = slot;
     p.scores = scores;
+    p.trace = c->trace;
     p.B = g.batch;
     p.Hq = g.num_q_heads;
     p.Hkv = g.num_kv_heads;

@@ -1,0 +1,59 @@
+"""Debug: run one decode step of a bench workload with the -DLF_TRACE build and summarise the
+per-unit event timeline (ns).  usage: LF_LIB=altlib/lib_trace.so python tools/trace_run.py r"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from bench import workload_of
+from lf_synth import Synth, random_cache
+from paper_2603_11504_b200 import Cache
+
+w = sys.argv[1] if len(sys.argv) > 1 else "r"
+wl = workload_of(w)
+cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype="bf16")
+plan = cache.plan()
+K, V, nv = cache.views()
+k0, v0 = random_cache(wl.B, wl.Hkv, wl.N, wl.d, device="cuda")
+K.copy_(k0); V.copy_(v0); nv.fill_(wl.N)
+del k0, v0
+syn = Synth(wl, device="cuda")
+q, kn, vn = syn.step()
+out, slot, _ = cache.new_outputs()
+ctas = 148 * 2
+tr = torch.zeros(ctas * 64 * 8, dtype=torch.int64, device="cuda")
+for i in range(3):
+    cache.decode_step(q, kn, vn, out, slot)
+cache.set_trace(tr)
+cache.decode_step(q, kn, vn, out, slot)
+torch.cuda.synchronize()
+a = tr.view(ctas, 64, 8).cpu().numpy().astype(np.int64)
+np.save(f"gpurun_out/trace_{w}.npy", a)
+used = a[:, :, 0] > 0
+t0 = a[used][:, 0].min()
+print("plan", plan, "ctas with events", int(used.any(axis=1).sum()))
+names = ["start", "Kdone", "Vdone", "xready", "scores", "fin", "prodQ", "mmaQ"]
+rows = a[used].astype(np.float64)
+for i, j in [(0, 1), (1, 2), (2, 3), (3, 4)]:
+    d = rows[:, j] - rows[:, i]
+    print(f"{names[i]}->{names[j]}: mean {d.mean()/1e3:.2f} us  p50 {np.median(d)/1e3:.2f}  max {d.max()/1e3:.2f}")
+# unit-to-unit gap: next unit start - this unit xready/scores
+per_cta = []
+for c in range(ctas):
+    u = np.nonzero(used[c])[0]
+    if len(u) < 2:
+        continue
+    ev = a[c, u].astype(np.float64)
+    per_cta.append(ev)
+    if c < 3:
+        print("cta", c, "units", len(u))
+        for k in range(min(len(u), 4)):
+            print("   ", " ".join(f"{names[i]}={ (ev[k, i]-t0)/1e3:8.2f}" for i in range(8) if ev[k, i] > 0))
+gaps = np.concatenate([ev[1:, 0] - ev[:-1, 4] for ev in per_cta])
+print(f"scores(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
+unit = np.concatenate([ev[1:, 0] - ev[:-1, 0] for ev in per_cta])
+print(f"unit period: mean {unit.mean()/1e3:.2f} us  p50 {np.median(unit)/1e3:.2f}")
+ends = np.array([ev[-1, 4] for ev in per_cta])
+print(f"kernel span {(ends.max()-t0)/1e3:.1f} us; last-unit end spread {(ends.max()-ends.min())/1e3:.1f} us; first start spread {(a[used][:,0].max()-t0)/1e3:.1f}")
