@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
                     if (g < G) {
-                        const float pv = valid ? exp2f(X[g * chunk + tok] - m[g]) : 0.f;
+                        const float pv = valid ? ptx::ex2_approx(X[g * chunk + tok] - m[g]) : 0.f;
                         z[g] += pv;
                         const uint16_t hi = f32_to_bf16_rne(pv);
                         const uint16_t lo = f32_to_bf16_rne(pv - bf16_to_f32(hi));
@@ -464,18 +464,14 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     const uint32_t ra = ptx::mapa(xc_addr, r);
                     const float mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
                     const float zr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, z) + 4 * g);
-                    Z += zr * exp2f(mr - M);
+                    Z += zr * ptx::ex2_approx(mr - M);   // same factors as the P and o combination
                 }
-                Z += exp2f(xs[g] - M);
+                Z += ptx::ex2_approx(xs[g] - M);
                 gM[g] = M;
                 gZ[g] = Z;
                 glz[g] = log2f(Z);
             }
             ptx::named_bar_sync(1, kNS);
-            if (s != 0 && sidx == 0) {   // done reading every rank's (m, Z): release them
-                ptx::fence_acq_rel_cluster();
-                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
-            }
             // ---- scores I_j (Eq. 6, mean over the group) and the local argmin key
             unsigned long long best = ~0ull;
             float wM[GP];
@@ -492,9 +488,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 }
                 float ssum = 0.f;
 #pragma unroll
-                for (int g = 0; g < GP; ++g) ssum += exp2f(av[g] - amax);
-                const float ls = log2f(lam) + amax + log2f(ssum) - log2G;   // log2 I_j, no underflow
-                if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * exp2f(amax) * ssum * invG;
+                for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
+                const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
+                if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
                 best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
             }
             if (p.scores)
@@ -511,8 +507,41 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 ptx::fence_acq_rel_cluster();
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
             }
+            // ---- output combine, split over the ranks: rank s owns elements [s*E, (s+1)*E), float4 each
+            {
+                const int E4 = (G * 32 + S - 1) / S;                     // float4 elements per rank
+                const int i4_0 = s * E4, i4_1 = min(G * 32, i4_0 + E4);
+                const uint16_t* vn = p.v_new + (size_t)u * 128;
+                for (int i4 = i4_0 + sidx; i4 < i4_1; i4 += kNS) {
+                    const int g = i4 >> 5, l = (i4 & 31) * 4;
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int r = 0; r < S; ++r) {
+                        const uint32_t ra = ptx::mapa(xc_addr, r);
+                        const float f = ptx::ex2_approx(ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g) - gM[g]);
+                        const float4 o4 = ptx::ld_dsmem_f32x4(ra + (uint32_t)offsetof(Xchg, o) + 16 * i4);
+                        acc.x = fmaf(o4.x, f, acc.x); acc.y = fmaf(o4.y, f, acc.y);
+                        acc.z = fmaf(o4.z, f, acc.z); acc.w = fmaf(o4.w, f, acc.w);
+                    }
+                    const float fn = ptx::ex2_approx(xs[g] - gM[g]);
+                    const uint2 vw = *(const uint2*)(vn + l);
+                    const float invZ = 1.0f / gZ[g];
+                    const float o0 = fmaf(fn, __uint_as_float(vw.x << 16), acc.x) * invZ;
+                    const float o1 = fmaf(fn, __uint_as_float(vw.x & 0xffff0000u), acc.y) * invZ;
+                    const float o2 = fmaf(fn, __uint_as_float(vw.y << 16), acc.z) * invZ;
+                    const float o3 = fmaf(fn, __uint_as_float(vw.y & 0xffff0000u), acc.w) * invZ;
+                    const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
+                    if (p.out_f32) {
+                        *(float4*)((float*)p.out + oi) = make_float4(o0, o1, o2, o3);
+                    } else {
+                        uint2 w;
+                        w.x = (uint32_t)f32_to_bf16_rne(o0) | ((uint32_t)f32_to_bf16_rne(o1) << 16);
+                        w.y = (uint32_t)f32_to_bf16_rne(o2) | ((uint32_t)f32_to_bf16_rne(o3) << 16);
+                        *(uint2*)((uint16_t*)p.out + oi) = w;
+                    }
+                }
+            }
             if (s == 0) {
-                // ---- rank 0: slot, output combine, in-place eviction write
+                // ---- rank 0: slot and the in-place eviction write
                 ptx::mbar_wait_cluster(BAR(KREADY + xp), use & 1u);
                 if (sidx == 0) {
                     unsigned long long mk = ~0ull;
@@ -525,21 +554,6 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 }
                 ptx::named_bar_sync(1, kNS);
                 const int sl = *s_slot;
-                const uint16_t* vn = p.v_new + (size_t)u * 128;
-                for (int i = sidx; i < G * 128; i += kNS) {
-                    const int g = i >> 7, l = i & 127;
-                    float acc = 0.f;
-                    for (int r = 0; r < S; ++r) {
-                        const uint32_t ra = ptx::mapa(xc_addr, r);
-                        const float mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
-                        acc += ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, o) + 4 * i) * exp2f(mr - gM[g]);
-                    }
-                    acc += exp2f(xs[g] - gM[g]) * bf16_to_f32(vn[l]);
-                    const float ov = acc / gZ[g];
-                    const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
-                    if (p.out_f32) ((float*)p.out)[oi] = ov;
-                    else ((uint16_t*)p.out)[oi] = f32_to_bf16_rne(ov);
-                }
                 // every CTA of the cluster consumed unit u's K/V before arriving on kready
                 if (sidx < 16) {
                     const size_t unit_off = (size_t)u * N * 128;
@@ -548,11 +562,11 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = ks[sidx];
                     ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = vs[sidx];
                 }
-                ptx::named_bar_sync(1, kNS);
-                if (sidx == 0) {
-                    ptx::fence_acq_rel_cluster();
-                    for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
-                }
+            }
+            ptx::named_bar_sync(1, kNS);   // this rank's remote reads of unit u are complete
+            if (sidx == 0) {
+                ptx::fence_acq_rel_cluster();
+                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
             }
         }
         // drain: no CTA leaves while a peer may still read its exchange buffers
