@@ -2,28 +2,29 @@
 //
 // Grid = C persistent clusters of S CTAs (1 CTA per SM).  Cluster c handles units
 // u = c, c + C, c + 2C, ... (unit = (sequence, kv head)); CTA s of the cluster owns slots
-// [s*chunk, (s+1)*chunk) of every unit.  Warp roles (320 threads):
+// [s*chunk, (s+1)*chunk) of every unit (chunk <= 4096).  Warp roles (64 + 128*kNG threads):
 //   warp 0     producer: Q rows of the next unit (LDG -> swizzled SMEM) and the K then V tiles
 //              (128 tokens x 128 d, two SWIZZLE_128B TMA boxes) through an ST-stage ring
-//   warp 1     TMEM allocator + tcgen05.mma issuer (one lane)
-//   warps 2-9  softmax / score / exchange warps in two groups of four that take alternate tiles
-//              (S and P buffers are double buffered by tile parity); warp w owns TMEM lanes
-//              [32(w%4), 32(w%4)+32)
-// The producer and MMA warps run ahead into the next unit while the softmax warps finish the
-// current one, so the HBM stream does not drain at unit boundaries.
+//   warp 1     TMEM allocator (all 512 columns) + tcgen05.mma issuer (one lane)
+//   warps 2..  kNG softmax groups of 4 warps; warp w owns TMEM lanes [32(w%4), 32(w%4)+32)
+//
+// TMEM-resident logits (hard part H1): S^T of every K tile of a unit stays in
+// TMEM (8 columns per 128-token tile, N = 8 MMA) until the unit's scores are final; two regions
+// alternate by unit parity, so the MMA streams the NEXT unit's whole K pass while the softmax
+// warps finalise the current one.  O^T (16 columns) lives at the start of the other region.
 //
 // Per unit (Alg. 1 P:500-547 restructured):
-//   K pass  S^T[128 tok x 16] = K_tile . Q^T (M=128, N=16, K=128, both K-major), fp32 in TMEM
-//           (double buffered); x_gj = S * scale * log2e -> SMEM, exact per-CTA max m_g (R5).
-//   V pass  P_g = 2^(x_g - m_g) as bf16 hi + lo (N = 16: 8 hi rows + 8 lo rows; bf16 P alone
-//           misses the 2e-3 out bar); O^T[128 d x 16] += V^T . P^T (M=128, N=16,
-//           K=16 tokens per MMA, A MN-major straight from the TMA tile); lambda_j = ||v_j||_1 from
-//           the same tile on the CUDA cores (Eq. 6, R9).  Rows past n are zeroed first.
-//   exchange (no cluster-wide barrier): each CTA publishes (m_g, Z_g, o_g) in its SMEM and
-//           arrives on every rank's `xready` mbarrier; after reading all (m, Z) it computes
-//           M_g, Z_g (incl. the current token), its scores and argmin key, arrives on rank 0's
-//           `kready`; rank 0 picks the slot (lowest index on ties), combines o, writes out,
-//           evicts in place (Fig. 2); `xfree` arrivals release the buffers.
+//   K pass  S^T[128 tok x 8] = K_tile . Q^T (M=128, N=8, K=128, both K-major SW128) -> TMEM.
+//   max     softmax groups read the unit's S from TMEM: exact per-CTA max m_g (R5).
+//   V pass  P_g = 2^(x_g - m_g), x = S * scale * log2e, as bf16 hi + lo (N = 16: 8 hi + 8 lo rows;
+//           bf16 P alone misses the 2e-3 out bar); O^T[128 d x 16] += V^T . P^T
+//           (M=128, N=16, K=16 tokens per MMA, A MN-major straight from the TMA tile);
+//           lambda_j = ||v_j||_1 from the same tile on the CUDA cores (Eq. 6, R9).
+//   exchange (no cluster-wide barrier): each CTA publishes (m_g, Z_g, o_g) in SMEM and arrives on
+//           every rank's `xready`; all ranks compute M_g, Z_g (incl. the current token),
+//           their scores I_j (from TMEM S) and argmin key -> rank 0's `kready`; the ranks split the
+//           output combine; rank 0 picks the slot (lowest index on ties) and evicts in place
+//           (Fig. 2); `xfree` arrivals release the exchange buffers.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -33,15 +34,15 @@
 namespace lf {
 namespace {
 
-constexpr int kNG = 3;                  // softmax warp groups (4 warps each), alternate tiles
+constexpr int kNG = 3;                  // softmax warp groups (4 warps each)
 constexpr int kNT = 64 + 128 * kNG;     // + producer warp + MMA warp
 constexpr int kNS = 128 * kNG;          // softmax threads
-constexpr int kStageBytes = 32768;   // 128 tokens x 128 d x bf16 (two 16 KB boxes)
+constexpr int kStageBytes = 32768;      // 128 tokens x 128 d x bf16 (two 16 KB boxes)
 constexpr int kBoxBytes = 16384;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxStages = 6;
-constexpr uint32_t kTmemCols = (kNG * 16 + 16) <= 64 ? 64 : 128;   // S per group (16 each) + O (16)
-constexpr uint32_t kOCol = kNG * 16;
+constexpr int kMaxChunk = 4096;         // 2 regions x 32 tiles x 8 columns = 512 TMEM columns
+constexpr uint32_t kTmemCols = 512;
 
 struct TcArgs {
     CUtensorMap tmK;
@@ -61,20 +62,19 @@ struct Xchg {
 };
 
 struct TcSmem {
-    int ring, q, pbuf, X, L, xb, misc, red, bars, tmem, total;
+    int ring, q, pbuf, L, xb, misc, red, bars, tmem, total;
 };
-__host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
+__host__ __device__ inline TcSmem tc_smem(int chunk, int stages) {
     TcSmem s;
     int off = 0;
     s.ring = off; off += stages * kStageBytes;   // 1024-aligned (swizzle atoms)
-    s.q = off;    off += 2 * 4096;               // Q^T operand x2 (per unit parity): 16 rows x 128 d
+    s.q = off;    off += 2 * 4096;               // Q^T operand x2 (unit parity): 8 rows used
     s.pbuf = off; off += kNG * 4096;             // P^T operand per group: 16 rows x 128 tokens
-    s.X = off;    off += G * chunk * 4;          // x_gj of the current unit
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 128 * 4;
     s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
-    s.bars = off; off += 40 * 8;
+    s.bars = off; off += 48 * 8;
     s.tmem = off; off += 16;
     s.total = off + 1024;                        // slack for 1024-byte alignment of the base
     return s;
@@ -83,10 +83,11 @@ __host__ __device__ inline TcSmem tc_smem(int G, int chunk, int stages) {
 // mbarrier slots
 constexpr int FULL = 0;                 // [kMaxStages]
 constexpr int EMPTY = FULL + kMaxStages;
-constexpr int SFULL = EMPTY + kMaxStages, SFREE = SFULL + kNG, PREADY = SFREE + kNG, PFREE = PREADY + kNG;
-constexpr int QFULL = PFREE + kNG, QFREE = QFULL + 2, OFULL = QFREE + 2, OFREE = OFULL + 1;
+constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kNG;
+constexpr int QFULL = PFREE + kNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
+constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
-static_assert(NBARS <= 40, "barrier slots");
+static_assert(NBARS <= 48, "barrier slots");
 
 // Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][8] u64.
 #ifdef LF_TRACE
@@ -134,8 +135,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int G = p.G, N = p.N, chunk = p.chunk, ST = a.stages;
-    const TcSmem so = tc_smem(G, chunk, ST);
-    float* X = (float*)(smem + so.X);
+    const TcSmem so = tc_smem(chunk, ST);
     float* Ls = (float*)(smem + so.L);
     Xchg* xb = (Xchg*)(smem + so.xb);
     float* misc = (float*)(smem + so.misc);
@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     const uint32_t pbuf = ptx::smem_u32(smem + so.pbuf);
     const uint32_t bars = ptx::smem_u32(smem + so.bars);
     auto BAR = [&](int i) { return bars + 8u * (uint32_t)i; };
+    // TMEM regions: S of unit parity `par` at column par*RC (8 columns per tile); O^T of unit
+    // parity `par` at the first 16 columns of region par^1
+    const int tmax = (chunk + 127) / 128;
+    const uint32_t RC = 8u * (uint32_t)(tmax > 2 ? tmax : 2);
 
     cg::cluster_group cluster = cg::this_cluster();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -157,17 +161,17 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
             ptx::mbar_init(BAR(FULL + i), 1);      // producer's expect_tx arrival
-            ptx::mbar_init(BAR(EMPTY + i), 1);     // MMA commit (the MMA is the stage's last reader)
+            ptx::mbar_init(BAR(EMPTY + i), 1);     // MMA commit (the MMA is each stage's last reader)
         }
         for (int i = 0; i < kNG; ++i) {
-            ptx::mbar_init(BAR(SFULL + i), 1);
-            ptx::mbar_init(BAR(SFREE + i), 4);
             ptx::mbar_init(BAR(PREADY + i), 4);
             ptx::mbar_init(BAR(PFREE + i), 1);
         }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(BAR(QFULL + i), 1);
             ptx::mbar_init(BAR(QFREE + i), 1);
+            ptx::mbar_init(BAR(KDONE + i), 1);
+            ptx::mbar_init(BAR(SFREE + i), 4 * kNG);
             ptx::mbar_init(BAR(XREADY + i), S);    // one arrival per rank
             ptx::mbar_init(BAR(KREADY + i), S);
             ptx::mbar_init(BAR(XFREE + i), S);
@@ -179,7 +183,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         ptx::tma_prefetch_desc(&a.tmV);
     }
     if (warp == 1) ptx::tmem_alloc<kTmemCols>(ptx::smem_u32(smem + so.tmem));
-    if (warp >= 2) {   // zero both Q and both P operand buffers (rows >= G stay zero)
+    if (warp >= 2) {   // zero the Q and P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
         for (int e = tid - 64; e < (2 + kNG) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
         ptx::fence_proxy_async_smem();
@@ -196,12 +200,12 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             const UnitInfo x = unit_info(p, u, s);
             const int qb = qi & 1;
             ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
-            // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ (g%8) of box c/8
+            // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
             const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
             unsigned char* qd = smem + so.q + qb * 4096;
             for (int e = lane; e < G * 16; e += 32) {
                 const int g = e >> 4, c = e & 15;
-                *(uint4*)(qd + (c >> 3) * 2048 + g * 128 + (((c & 7) ^ (g & 7)) << 4)) = __ldg(qg + e);
+                *(uint4*)(qd + (c >> 3) * 1024 + g * 128 + (((c & 7) ^ g) << 4)) = __ldg(qg + e);
             }
             ptx::fence_proxy_async_smem();
             __syncwarp();
@@ -225,33 +229,35 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------------------------
         if (lane == 0) {
-            constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 16, 0, 0);
+            constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
-            uint32_t it = 0, si = 0, pi = 0, ui = 0;
+            uint32_t it = 0, pi = 0, ui = 0;
             for (int u = cid; u < units; u += C, ++ui) {
                 const UnitInfo x = unit_info(p, u, s);
-                const int qb = ui & 1;
-                ptx::mbar_wait(BAR(QFULL + qb), (ui >> 1) & 1u);
+                const uint32_t par = ui & 1u;
+                ptx::mbar_wait(BAR(QFULL + par), (ui >> 1) & 1u);
+                ptx::mbar_wait(BAR(SFREE + par), ((ui >> 1) & 1u) ^ 1u);   // unit ui-2 finalised
+                ptx::mbar_wait(BAR(OFREE), (ui & 1u) ^ 1u);                  // O(ui-1) drained
                 LF_EVENT(ui, 7);
-                const uint32_t qbase = qsm + (uint32_t)qb * 4096;
-                for (int t = 0; t < x.ntiles; ++t, ++it, ++si) {          // S^T = K_tile . Q^T
+                ptx::tc_fence_after();
+                const uint32_t qbase = qsm + par * 4096;
+                const uint32_t sreg = tmem + par * RC;
+                for (int t = 0; t < x.ntiles; ++t, ++it) {                  // S^T = K_tile . Q^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    const int sb = si % kNG;
-                    ptx::mbar_wait(BAR(SFREE + sb), ((si / kNG) & 1u) ^ 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
 #pragma unroll
                     for (int kk = 0; kk < 8; ++kk) {
                         const uint64_t da = ptx::smem_desc_sw128(base + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
-                        const uint64_t db = ptx::smem_desc_sw128(qbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                        ptx::mma_bf16(tmem + (uint32_t)sb * 16, da, db, idesc_qk, kk > 0);
+                        const uint64_t db = ptx::smem_desc_sw128(qbase + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 1024);
+                        ptx::mma_bf16(sreg + 8u * (uint32_t)t, da, db, idesc_qk, kk > 0);
                     }
-                    ptx::mma_commit(BAR(SFULL + sb));
                     ptx::mma_commit(BAR(EMPTY + st));
                 }
-                ptx::mma_commit(BAR(QFREE + qb));
-                ptx::mbar_wait(BAR(OFREE), (ui & 1u) ^ 1u);               // previous O drained
+                ptx::mma_commit(BAR(QFREE + par));
+                ptx::mma_commit(BAR(KDONE + par));
+                const uint32_t oreg = tmem + (par ^ 1u) * RC;
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
@@ -264,7 +270,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     for (int kk = 0; kk < 8; ++kk) {
                         const uint64_t da = ptx::smem_desc_sw128(base + kk * 2048, kBoxBytes, 1024);
                         const uint64_t db = ptx::smem_desc_sw128(pbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                        ptx::mma_bf16(tmem + kOCol, da, db, idesc_pv, (t | kk) > 0);
+                        ptx::mma_bf16(oreg, da, db, idesc_pv, (t | kk) > 0);
                     }
                     ptx::mma_commit(BAR(EMPTY + st));
                     ptx::mma_commit(BAR(PFREE + pb));
@@ -275,7 +281,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         __syncwarp();
     } else {
         // ------------------------------ softmax / score / exchange warps -------------------------
-        const int grp = (warp - 2) >> 2;              // two groups take alternate tiles
+        const int grp = (warp - 2) >> 2;              // groups take tiles round-robin
         const int q4 = warp & 3;
         const int sidx = tid - 64;                    // 0 .. kNS-1
         const int row = 32 * q4 + lane;               // token row of a tile / d index of O
@@ -289,10 +295,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         const int box = row >> 6, cc = row & 63;
         const float log2G = log2f((float)G);
         const float invG = 1.0f / (float)G;
-        uint32_t it = 0, si = 0, pi = 0, ui = 0;
+        const float sl2 = p.scale_log2;
+        uint32_t it = 0, pi = 0, ui = 0;
         for (int u = cid; u < units; u += C, ++ui) {
             const UnitInfo x = unit_info(p, u, s);
             const int nv = x.nv;
+            const uint32_t par = ui & 1u;
+            const uint32_t sreg = tl + par * RC;
             if (sidx == 0) LF_EVENT(ui, 0);
             // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
             for (int g = warp - 2; g < G; g += 4 * kNG) {
@@ -303,36 +312,24 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                if (lane == 0) xs[g] = acc * p.scale_log2;
+                if (lane == 0) xs[g] = acc * sl2;
             }
-            // ---- K pass: logits to SMEM, running max
+            // ---- max over the unit's logits (TMEM-resident S)
+            ptx::mbar_wait(BAR(KDONE + par), (ui >> 1) & 1u);
+            ptx::tc_fence_after();
             float mloc[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
-            for (int t = 0; t < x.ntiles; ++t) {
-                const uint32_t c = si + t;
-                if ((int)(c % kNG) != grp) continue;
-                const int st = (it + t) % ST, sb = c % kNG;
-                ptx::mbar_wait(BAR(SFULL + sb), (c / kNG) & 1u);
-                ptx::tc_fence_after();
+            for (int t = grp; t < x.ntiles; t += kNG) {
                 uint32_t r[8];
-                ptx::tmem_ld_x8(tl + (uint32_t)sb * 16, r);
+                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
                 ptx::tmem_ld_wait();
-                const int tok = t * 128 + row;
-                const bool valid = tok < nv;
+                if (t * 128 + row < nv) {
 #pragma unroll
-                for (int g = 0; g < GP; ++g) {
-                    if (g < G) {
-                        const float xv = valid ? __uint_as_float(r[g]) * p.scale_log2 : -INFINITY;
-                        X[g * chunk + tok] = xv;
-                        mloc[g] = fmaxf(mloc[g], xv);
-                    }
+                    for (int g = 0; g < GP; ++g)
+                        if (g < G) mloc[g] = fmaxf(mloc[g], __uint_as_float(r[g]) * sl2);
                 }
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(BAR(SFREE + sb));
             }
-            si += x.ntiles;
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
 #pragma unroll
@@ -359,14 +356,17 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 const uint32_t c = pi + t;
                 if ((int)(c % kNG) != grp) continue;
                 const int pb = c % kNG;
+                uint32_t r[8];
+                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
                 ptx::mbar_wait(BAR(PFREE + pb), ((c / kNG) & 1u) ^ 1u);
+                ptx::tmem_ld_wait();
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
                 unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
                     if (g < G) {
-                        const float pv = valid ? ptx::ex2_approx(X[g * chunk + tok] - m[g]) : 0.f;
+                        const float pv = valid ? ptx::ex2_approx(__uint_as_float(r[g]) * sl2 - m[g]) : 0.f;
                         z[g] += pv;
                         const uint16_t hi = f32_to_bf16_rne(pv);
                         const uint16_t lo = f32_to_bf16_rne(pv - bf16_to_f32(hi));
@@ -382,8 +382,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
 #pragma unroll
                     for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            *(uint4*)(Vt + bb * kBoxBytes + row * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+                        for (int k = 0; k < 8; ++k)
+                            *(uint4*)(Vt + bb * kBoxBytes + row * 128 + k * 16) = make_uint4(0, 0, 0, 0);
                 }
                 // lambda_j from the landed tile, before PREADY: after the PV MMA the stage is refilled
                 float lam = 0.f;
@@ -391,8 +391,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
 #pragma unroll
                     for (int bb = 0; bb < 2; ++bb)
 #pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((c ^ (row & 7)) << 4)));
+                        for (int k = 0; k < 8; ++k)
+                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)));
                 }
                 Ls[tok] = lam;
                 ptx::fence_proxy_async_smem();
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 ptx::tc_fence_after();
                 if (x.ntiles > 0) {
                     uint32_t o[16];
-                    ptx::tmem_ld_x16(tl + kOCol, o);
+                    ptx::tmem_ld_x16(tl + (par ^ 1u) * RC, o);
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int g = 0; g < GP; ++g)
@@ -472,27 +472,36 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 glz[g] = log2f(Z);
             }
             ptx::named_bar_sync(1, kNS);
-            // ---- scores I_j (Eq. 6, mean over the group) and the local argmin key
+            // ---- scores I_j (Eq. 6, mean over the group) from the TMEM logits; local argmin key
             unsigned long long best = ~0ull;
             float wM[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
-            for (int j = sidx; j < nv; j += kNS) {
-                const float lam = Ls[j];
-                float av[GP];
-                float amax = -INFINITY;
+            for (int t = grp; t < x.ntiles; t += kNG) {
+                uint32_t r[8];
+                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
+                ptx::tmem_ld_wait();
+                const int j = t * 128 + row;
+                if (j < nv) {
+                    const float lam = Ls[j];
+                    float av[GP];
+                    float amax = -INFINITY;
 #pragma unroll
-                for (int g = 0; g < GP; ++g) {
-                    av[g] = g < G ? X[g * chunk + j] - wM[g] : -INFINITY;
-                    amax = fmaxf(amax, av[g]);
+                    for (int g = 0; g < GP; ++g) {
+                        av[g] = g < G ? __uint_as_float(r[g]) * sl2 - wM[g] : -INFINITY;
+                        amax = fmaxf(amax, av[g]);
+                    }
+                    float ssum = 0.f;
+#pragma unroll
+                    for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
+                    const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
+                    if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
+                    best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
                 }
-                float ssum = 0.f;
-#pragma unroll
-                for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
-                const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
-                if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
-                best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
             }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(BAR(SFREE + par));          // S(ui) no longer read
             if (p.scores)
                 for (int j = nv + sidx; j < x.c1 - x.c0; j += kNS) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
 #pragma unroll
@@ -507,9 +516,9 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 ptx::fence_acq_rel_cluster();
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
             }
-            // ---- output combine, split over the ranks: rank s owns elements [s*E, (s+1)*E), float4 each
+            // ---- output combine, split over the ranks: rank s owns float4 elements [s*E4, (s+1)*E4)
             {
-                const int E4 = (G * 32 + S - 1) / S;                     // float4 elements per rank
+                const int E4 = (G * 32 + S - 1) / S;
                 const int i4_0 = s * E4, i4_1 = min(G * 32, i4_0 + E4);
                 const uint16_t* vn = p.v_new + (size_t)u * 128;
                 for (int i4 = i4_0 + sidx; i4 < i4_1; i4 += kNS) {
@@ -672,8 +681,8 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t rows, int d) {
     return r == CUDA_SUCCESS;
 }
 
-int stages_for(int G, int chunk) {
-    const int base = tc_smem(G, chunk, 0).total;
+int stages_for(int chunk) {
+    const int base = tc_smem(chunk, 0).total;
     int st = (kSmemLimit - base) / kStageBytes;
     return st > kMaxStages ? kMaxStages : st;
 }
@@ -682,8 +691,8 @@ int stages_for(int G, int chunk) {
 
 bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 
-// Split plan: for each cluster size S in {1, 2, 4, 8, 16} whose chunk leaves room for >= 3 ring
-// stages beside X and lambda, the persistent grid holds C_S = cudaOccupancyMaxActiveClusters
+// Split plan: for each cluster size S in {1, 2, 4, 8, 16} whose chunk (<= 4096 tokens: two TMEM
+// logit regions) leaves room for >= 3 ring stages, the persistent grid holds C_S = cudaOccupancyMaxActiveClusters
 // clusters (capped at the unit count) and needs ceil(units / C_S) rounds of `chunk` tokens per
 // CTA; the plan minimises rounds * (chunk + 256)  (256 tokens ~ the per-unit exchange overhead).
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
@@ -702,10 +711,11 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         const int chunk = split_tokens > 0 ? split_tokens : ((Nr + S - 1) / S + 127) / 128 * 128;
         const int splits = (N + chunk - 1) / chunk;
         if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
-        if (splits > 16) continue;
-        const int st = stages_for(G, chunk);
+        if (splits > 16 || chunk > kMaxChunk) continue;
+        const int st = stages_for(chunk);
         if (st < 3) continue;
-        const int smem = tc_smem(G, chunk, st).total;
+        // >= 120 KB keeps one CTA per SM: each CTA allocates all 512 TMEM columns
+        const int smem = max(tc_smem(chunk, st).total, 120 * 1024);
         const int C = gpad_tc(G) == 4 ? max_active_clusters<4>(splits, smem) : max_active_clusters<8>(splits, smem);
         if (C <= 0) continue;
         const int Cu = C < units ? C : units;
