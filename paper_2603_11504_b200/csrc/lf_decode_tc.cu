@@ -694,7 +694,8 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 // Split plan: for each cluster size S in {1, 2, 4, 8, 16} whose chunk (<= 4096 tokens: two TMEM
 // logit regions) leaves room for >= 3 ring stages, the persistent grid holds C_S = cudaOccupancyMaxActiveClusters
 // clusters (capped at the unit count) and needs ceil(units / C_S) rounds of `chunk` tokens per
-// CTA; the plan minimises rounds * (chunk + 256)  (256 tokens ~ the per-unit exchange overhead).
+// CTA; the plan minimises rounds * (chunk + overhead), the overhead (in streamed tokens) being the
+// measured unit-boundary cost: ~128 tokens alone, ~1024 with the cross-CTA exchange (S > 1).
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     (void)d;
     (void)num_sms;
@@ -720,7 +721,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         if (C <= 0) continue;
         const int Cu = C < units ? C : units;
         const long long rounds = (units + Cu - 1) / Cu;
-        const long long cost = rounds * (chunk + 256);
+        const long long cost = rounds * (chunk + (splits > 1 ? 1024 : 128));   // exchange cost for S > 1
         if (best_cost < 0 || cost < best_cost) {
             best_cost = cost;
             best.splits = splits;
