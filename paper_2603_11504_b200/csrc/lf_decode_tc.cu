@@ -89,14 +89,14 @@ constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 48, "barrier slots");
 
-// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][8] u64.
+// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][16] u64.
 #ifdef LF_TRACE
 #define LF_EVENT(ui_, slot_)                                                                   \
     do {                                                                                       \
         if (p.trace) {                                                                         \
             unsigned long long t_;                                                             \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-            p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 8 + (slot_)] = t_;              \
+            p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 16 + (slot_)] = t_;             \
         }                                                                                      \
     } while (0)
 #else
@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                 if (lane == 0) xs[g] = acc * sl2;
             }
+            if (sidx == 0) LF_EVENT(ui, 15);
             // ---- max over the unit's logits (TMEM-resident S)
             ptx::mbar_wait(BAR(KDONE + par), (ui >> 1) & 1u);
             ptx::tc_fence_after();
@@ -416,8 +417,10 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             const uint32_t use = ui >> 1;
             Xchg* xc = xb + xp;
             ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // readers of its last use are done
+            if (sidx == 0) LF_EVENT(ui, 8);
             if (grp == 0) {   // group 0 drains O (TMEM lane = d)
                 ptx::mbar_wait(BAR(OFULL), ui & 1u);
+                if (sidx == 0) LF_EVENT(ui, 9);
                 ptx::tc_fence_after();
                 if (x.ntiles > 0) {
                     uint32_t o[16];
@@ -434,6 +437,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
             }
             ptx::named_bar_sync(1, kNS);                                // red[] and xc->o complete
+            if (sidx == 0) LF_EVENT(ui, 10);
             if (sidx < G) {
                 const int g = sidx;
                 float mm = red[g], zz = red[kNG * 64 + g];
@@ -446,6 +450,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             }
             ptx::named_bar_sync(1, kNS);
             const uint32_t xr_local = BAR(XREADY + xp);
+            if (sidx == 0) LF_EVENT(ui, 11);
             if (sidx == 0) {
                 ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(xr_local, r));
@@ -472,6 +477,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 glz[g] = log2f(Z);
             }
             ptx::named_bar_sync(1, kNS);
+            if (sidx == 0) LF_EVENT(ui, 12);
             // ---- scores I_j (Eq. 6, mean over the group) from the TMEM logits; local argmin key
             unsigned long long best = ~0ull;
             float wM[GP];
@@ -549,6 +555,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     }
                 }
             }
+            if (sidx == 0) LF_EVENT(ui, 13);
             if (s == 0) {
                 // ---- rank 0: slot and the in-place eviction write
                 ptx::mbar_wait_cluster(BAR(KREADY + xp), use & 1u);
@@ -573,6 +580,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 }
             }
             ptx::named_bar_sync(1, kNS);   // this rank's remote reads of unit u are complete
+            if (sidx == 0) LF_EVENT(ui, 14);
             if (sidx == 0) {
                 ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));

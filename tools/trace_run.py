@@ -23,21 +23,25 @@ syn = Synth(wl, device="cuda")
 q, kn, vn = syn.step()
 out, slot, _ = cache.new_outputs()
 ctas = 148 * 2
-tr = torch.zeros(ctas * 64 * 8, dtype=torch.int64, device="cuda")
+tr = torch.zeros(ctas * 64 * 16, dtype=torch.int64, device="cuda")
 for i in range(3):
     cache.decode_step(q, kn, vn, out, slot)
 cache.set_trace(tr)
 cache.decode_step(q, kn, vn, out, slot)
 torch.cuda.synchronize()
-a = tr.view(ctas, 64, 8).cpu().numpy().astype(np.int64)
+a = tr.view(ctas, 64, 16).cpu().numpy().astype(np.int64)
 np.save(f"gpurun_out/trace_{w}.npy", a)
 used = a[:, :, 0] > 0
 t0 = a[used][:, 0].min()
 print("plan", plan, "ctas with events", int(used.any(axis=1).sum()))
-names = ["start", "Kdone", "Vdone", "xready", "scores", "fin", "prodQ", "mmaQ"]
+names = ["start", "maxdone", "Vdone", "xready", "scores", "fin", "prodQ", "mmaQ", "xfree", "ofull",
+         "obar", "mz", "MZ", "comb", "r0done", "xsdone"]
 rows = a[used].astype(np.float64)
-for i, j in [(0, 1), (1, 2), (2, 3), (3, 4)]:
-    d = rows[:, j] - rows[:, i]
+for i, j in [(0, 15), (15, 1), (1, 2), (2, 8), (8, 9), (9, 10), (10, 11), (11, 3), (3, 12), (12, 4), (4, 13), (13, 14)]:
+    ok = (rows[:, j] > 0) & (rows[:, i] > 0)
+    d = rows[ok, j] - rows[ok, i]
+    if not ok.any():
+        continue
     print(f"{names[i]}->{names[j]}: mean {d.mean()/1e3:.2f} us  p50 {np.median(d)/1e3:.2f}  max {d.max()/1e3:.2f}")
 # unit-to-unit gap: next unit start - this unit xready/scores
 per_cta = []
@@ -50,9 +54,9 @@ for c in range(ctas):
     if c < 3:
         print("cta", c, "units", len(u))
         for k in range(min(len(u), 4)):
-            print("   ", " ".join(f"{names[i]}={ (ev[k, i]-t0)/1e3:8.2f}" for i in range(8) if ev[k, i] > 0))
-gaps = np.concatenate([ev[1:, 0] - ev[:-1, 4] for ev in per_cta])
-print(f"scores(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
+            print("   ", " ".join(f"{names[i]}={ (ev[k, i]-t0)/1e3:.2f}" for i in range(16) if ev[k, i] > 0))
+gaps = np.concatenate([ev[1:, 0] - ev[:-1, 14] for ev in per_cta])
+print(f"r0done(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
 unit = np.concatenate([ev[1:, 0] - ev[:-1, 0] for ev in per_cta])
 print(f"unit period: mean {unit.mean()/1e3:.2f} us  p50 {np.median(unit)/1e3:.2f}")
 ends = np.array([ev[-1, 4] for ev in per_cta])
