@@ -62,7 +62,7 @@ struct Xchg {
 };
 
 struct TcSmem {
-    int ring, q, pbuf, L, xb, misc, red, bars, tmem, total;
+    int ring, q, pbuf, L, xb, misc, kvn, red, bars, tmem, total;
 };
 __host__ __device__ inline TcSmem tc_smem(int chunk, int stages) {
     TcSmem s;
@@ -73,6 +73,7 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages) {
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 128 * 4;
+    s.kvn = off;  off += 2 * 256;                // k_new, v_new rows of the current unit
     s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
     s.bars = off; off += 48 * 8;
     s.tmem = off; off += 16;
@@ -303,6 +304,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             const uint32_t par = ui & 1u;
             const uint32_t sreg = tl + par * RC;
             if (sidx == 0) LF_EVENT(ui, 0);
+            // stage the current token's k*, v* rows (combine + eviction write read them later)
+            uint4* kvn = (uint4*)(smem + so.kvn);
+            if (warp == 2 + 4 * kNG - 1) {
+                const uint4* src = lane < 16 ? (const uint4*)(p.k_new + (size_t)u * 128) + lane
+                                             : (const uint4*)(p.v_new + (size_t)u * 128) + (lane - 16);
+                kvn[lane] = __ldg(src);
+            }
             // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
             for (int g = warp - 2; g < G; g += 4 * kNG) {
                 const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
@@ -452,7 +460,6 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) LF_EVENT(ui, 11);
             if (sidx == 0) {
-                ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(xr_local, r));
             }
             ptx::mbar_wait_cluster(xr_local, use & 1u);
@@ -519,14 +526,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 unsigned long long kb = kred[0];
                 for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
                 xc->key = kb;
-                ptx::fence_acq_rel_cluster();
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
             }
             // ---- output combine, split over the ranks: rank s owns float4 elements [s*E4, (s+1)*E4)
             {
                 const int E4 = (G * 32 + S - 1) / S;
                 const int i4_0 = s * E4, i4_1 = min(G * 32, i4_0 + E4);
-                const uint16_t* vn = p.v_new + (size_t)u * 128;
+                const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
                 for (int i4 = i4_0 + sidx; i4 < i4_1; i4 += kNS) {
                     const int g = i4 >> 5, l = (i4 & 31) * 4;
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -573,16 +579,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 // every CTA of the cluster consumed unit u's K/V before arriving on kready
                 if (sidx < 16) {
                     const size_t unit_off = (size_t)u * N * 128;
-                    const uint4* ks = (const uint4*)(p.k_new + (size_t)u * 128);
-                    const uint4* vs = (const uint4*)(p.v_new + (size_t)u * 128);
-                    ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = ks[sidx];
-                    ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = vs[sidx];
+                    ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = kvn[sidx];
+                    ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = kvn[16 + sidx];
                 }
             }
             ptx::named_bar_sync(1, kNS);   // this rank's remote reads of unit u are complete
             if (sidx == 0) LF_EVENT(ui, 14);
             if (sidx == 0) {
-                ptx::fence_acq_rel_cluster();
                 for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
             }
         }
