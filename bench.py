@@ -124,10 +124,8 @@ class ClockSampler:
 
 
 def dist_env():
-    ws = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return ws, rank, local
+    from paper_2603_11504_b200 import dist as lfd
+    return lfd.env()
 
 
 # ------------------------------------------------------------------------------------------------
@@ -254,7 +252,8 @@ def main():
         print(f"warning: WORLD_SIZE={ws} != --gpus {args.gpus}", file=sys.stderr)
     args.gpus = max(ws, 1) if ws > 1 else args.gpus
     wl = workload_of(args.workload)
-    B_total = wl.B * args.gpus if args.scaling == "weak" else wl.B
+    from paper_2603_11504_b200 import dist as lfd
+    B, b0, B_total = lfd.shard(wl.B, args.gpus, rank, args.scaling)
     if args.impl == "reference":
         return run_reference(args, wl, B_total)
     if args.gpus > 1 and ws == 1:
@@ -269,10 +268,6 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
-    if B_total % args.gpus:
-        raise SystemExit("global batch not divisible by the GPU count")
-    B = B_total // args.gpus
-    b0 = rank * B
 
     cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
                   split_tokens=args.split_tokens, device=local)
@@ -324,14 +319,19 @@ def main():
     if pg:
         pg.barrier()
     ms = ev0.elapsed_time(ev1)
-    ms_t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    ms_max = lfd.max_over_ranks(ms, device=dev)
+    gather = None
     if pg:
-        pg.all_reduce(ms_t, op=pg.ReduceOp.MAX)
-        # statistics gather (off the hot path): per-rank slot checksums
-        chk = torch.tensor([float(slot.double().sum())], device=dev, dtype=torch.float64)
-        allchk = [torch.zeros_like(chk) for _ in range(ws)]
-        pg.all_gather(allchk, chk)
-    ms_max = float(ms_t.item())
+        # off the hot path: gather every rank's out / slot over NCCL (NVLink) and time it
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        out_all = lfd.gather_rows(out)
+        slot_all = lfd.gather_rows(slot)
+        g1.record()
+        torch.cuda.synchronize(dev)
+        gather = {"us": lfd.max_over_ranks(g0.elapsed_time(g1) * 1e3, device=dev),
+                  "bytes": out_all.numel() * out_all.element_size() + slot_all.numel() * 4}
     ms_step = ms_max / args.steps
     value = B_total / (ms_step / 1e3)
 
@@ -353,9 +353,7 @@ def main():
         cache.decode_step_host(*hq, oh, sh, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev, dtype=torch.float64)
-    if pg:
-        pg.all_reduce(e_ms, op=pg.ReduceOp.MAX)
+    e_ms = torch.tensor([lfd.max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device=dev)])
     h2d = sum(t.numel() * t.element_size() for t in hq)
     d2h = oh.numel() * oh.element_size() + sh.numel() * 4
     e2e = {"value": B_total / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
@@ -383,6 +381,8 @@ def main():
         "clocks": clk.summary(),
         "graph": graph is not None,
     }
+    if gather:
+        line["nccl_gather_out_slot"] = gather
     if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
         v, cores, desc, sps = oracle_rate(wl, B_total, seconds=args.ref_seconds)
         line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc}
