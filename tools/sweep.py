@@ -1,0 +1,59 @@
+"""BASELINE configs[4]: budget sweep 512-16384 x batch 1-512 at fixed 80 % compression (32/8 GQA, d=128):
+latency and HBM GB/s per point (full cache, every step evicts), one JSON line per point.
+usage: python tools/sweep.py [--out gpurun_out/sweep.jsonl] [--steps 20]"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from bench import alg_bytes_per_step, peaks
+from lf_synth import Synth, random_cache, sweep_workload
+from paper_2603_11504_b200 import Cache
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
+ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--budgets", default="512,1024,2048,4096,8192,16384")
+ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256,512")
+args = ap.parse_args()
+peak, _ = peaks()
+f = open(args.out, "w")
+for N in map(int, args.budgets.split(",")):
+    for B in map(int, args.batches.split(",")):
+        wl = sweep_workload(B, N)
+        cache = Cache(B, wl.Hq, wl.Hkv, wl.d, N, out_dtype="bf16")
+        K, V, nv = cache.views()
+        k0, v0 = random_cache(B, wl.Hkv, N, wl.d, device="cuda")
+        K.copy_(k0); V.copy_(v0); nv.fill_(N)
+        del k0, v0
+        syn = Synth(wl, device="cuda")
+        pool = [syn.step() for _ in range(4)]
+        out, slot, _ = cache.new_outputs()
+        st = torch.cuda.Stream()
+        for i in range(5):
+            cache.decode_step(*pool[i % 4], out, slot, stream=st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(args.steps):
+                cache.decode_step(*pool[i % 4], out, slot, stream=st)
+        g.replay(); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / args.steps
+        alg = alg_bytes_per_step(wl, B, 2)
+        rec = {"B": B, "N": N, "latency_us": us, "tokens_per_s": B / (us * 1e-6), "alg_bytes": alg,
+               "GBps": alg / (us * 1e-6) / 1e9, "frac_measured_peak": alg / (us * 1e-6) / 1e9 / peak,
+               "plan": cache.plan()}
+        print(json.dumps(rec), flush=True)
+        f.write(json.dumps(rec) + "\n")
+        cache.close()
+        del cache, K, V, nv, pool, out, slot, g
+        torch.cuda.empty_cache()
