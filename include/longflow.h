@@ -53,7 +53,13 @@ typedef enum {
 typedef enum { LF_DTYPE_BF16 = 0, LF_DTYPE_F32 = 1 } lf_dtype;
 
 typedef enum {
-    LF_EVICT_SAME_STEP = 0  /* R1: the current token is attended, then covers the victim this step */
+    LF_EVICT_SAME_STEP = 0,                /* R1: the current token is attended, then covers the
+                                              victim chosen in this step (default)               */
+    LF_EVICT_DEFERRED = 1,                 /* Fig. 2 literal: the current token first covers
+                                              the slot chosen at the previous step (or is appended),
+                                              attention runs over the cache, every valid slot is a
+                                              candidate, the argmin is covered at the next step   */
+    LF_EVICT_DEFERRED_EXCLUDE_NEWEST = 2   /* as DEFERRED, the slot just written is not a candidate */
 } lf_evict_mode;
 
 typedef enum {
@@ -123,6 +129,11 @@ lf_status lf_cache_views(const lf_cache* c, void** k, void** v, int32_t** n_vali
  * unit (CTAs per cluster) and tokens per split. */
 lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
                         int32_t* split_tokens);
+
+/* Deferred modes: device view of int32 [B][Hkv], the slot the next step's token will cover
+ * (-1 = none yet).  In deferred modes lf_decode_step's `slot` returns where the current token
+ * was written, and `scores` covers every valid slot including it. */
+lf_status lf_cache_pending(const lf_cache* c, int32_t** pend);
 
 /* Number of CUDA kernels lf_decode_step launches per call (for launch accounting). */
 int32_t lf_kernels_per_step(const lf_cache* c);

@@ -24,7 +24,8 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 EXPORTS = ["lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
            "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_kernels_per_step",
-           "lf_debug_set_trace", "lf_status_string", "lf_last_error"]
+           "lf_debug_set_trace", "lf_cache_pending", "lf_status_string", "lf_last_error"]
+MODES = {"same_step": 0, "deferred": 1, "deferred_exclude_newest": 2}
 
 
 class LFError(RuntimeError):
@@ -61,6 +62,8 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_decode_step_host.argtypes = [P, P, P, P, P, P, P]
     lib.lf_cache_views.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.lf_cache_pending.argtypes = [P, ctypes.POINTER(P)]
+    lib.lf_cache_pending.restype = ctypes.c_int
     lib.lf_debug_set_trace.argtypes = [P, P]
     lib.lf_debug_set_trace.restype = ctypes.c_int
     lib.lf_kernels_per_step.argtypes = [P]
@@ -97,9 +100,9 @@ def _stream(stream):
 
 
 def make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32", softmax_scale=0.0,
-                kernel="auto", split_tokens=0) -> CacheConfig:
+                kernel="auto", split_tokens=0, mode="same_step") -> CacheConfig:
     return CacheConfig(batch, num_q_heads, num_kv_heads, head_dim, budget, DTYPES[out_dtype],
-                       float(softmax_scale), 0, KERNELS[kernel], split_tokens)
+                       float(softmax_scale), MODES[mode], KERNELS[kernel], split_tokens)
 
 
 def cache_bytes(cfg: CacheConfig) -> int:
@@ -116,10 +119,11 @@ class Cache:
     """
 
     def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32",
-                 softmax_scale=0.0, kernel="auto", split_tokens=0, device=0, library_owned=False):
+                 softmax_scale=0.0, kernel="auto", split_tokens=0, device=0, library_owned=False,
+                 mode="same_step"):
         lib = load()
         self.cfg = make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype, softmax_scale,
-                               kernel, split_tokens)
+                               kernel, split_tokens, mode)
         self.B, self.Hq, self.Hkv, self.d, self.N = batch, num_q_heads, num_kv_heads, head_dim, budget
         self.G = num_q_heads // num_kv_heads
         self.out_dtype = out_dtype
@@ -183,6 +187,14 @@ class Cache:
         V = sl(vp, kv).view(torch.bfloat16).view(self.B, self.Hkv, self.N, self.d)
         nv = sl(nvp, self.B * self.Hkv * 4).view(torch.int32).view(self.B, self.Hkv)
         return K, V, nv
+
+    def pending(self):
+        """Deferred modes: int32 [B][Hkv] torch view of the slot the next token will cover."""
+        pp = ctypes.c_void_p()
+        _check(load().lf_cache_pending(self._h, ctypes.byref(pp)), "lf_cache_pending")
+        base = self._buf.data_ptr()
+        return self._buf[pp.value - base:pp.value - base + self.B * self.Hkv * 4].view(torch.int32).view(
+            self.B, self.Hkv)
 
     def plan(self):
         k, s, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

@@ -77,7 +77,7 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
             for (int l = lane; l < D; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-            if (lane == 0) xnew[g] = acc * p.scale_log2;
+            if (lane == 0) xnew[g] = p.deferred ? -INFINITY : acc * p.scale_log2;
         }
     }
     cluster.sync();   // #1: every CTA's (m, Z, o) partials visible cluster-wide
@@ -101,6 +101,7 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
     unsigned long long best = ~0ull;
     const float log2G = log2f((float)G);
     const float invG = 1.0f / (float)G;
+    const int excl = (p.deferred && p.exclude_newest) ? p.written[u] : -1;
     for (int j = tid; j < nv; j += NT) {
         const float lam = lds_f32(t.L + j);
         float a[GP];
@@ -118,7 +119,7 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
         }
         const float ls = log2f(lam) + amax + log2f(ssum) - log2G;   // log2 I_j (no underflow)
         if (p.scores) p.scores[(size_t)u * N + c0 + j] = lam * sc * invG;
-        best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(c0 + j));
+        if (c0 + j != excl) best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(c0 + j));
     }
     if (p.scores)
         for (int j = nv + tid; j < c1 - c0; j += NT) p.scores[(size_t)u * N + c0 + j] = INFINITY;
@@ -137,10 +138,15 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
         if (tid == 0) {
             unsigned long long m = ~0ull;
             for (int r = 0; r < S; ++r) m = umin64(m, cluster.map_shared_rank(t.keys, r)[0]);
-            const int sl = n < N ? n : (int)(m & 0xffffffffull);
-            *s_slot = sl;
-            p.slot[u] = sl;
-            if (n < N) p.n_valid[u] = n + 1;
+            if (p.deferred) {            // next step's victim; the current token is already in place
+                p.pend[u] = (int)(m & 0xffffffffull);
+                *s_slot = -1;
+            } else {
+                const int sl = n < N ? n : (int)(m & 0xffffffffull);
+                *s_slot = sl;
+                p.slot[u] = sl;
+                if (n < N) p.n_valid[u] = n + 1;
+            }
         }
         __syncthreads();
         const int sl = *s_slot;
@@ -159,7 +165,7 @@ __device__ __forceinline__ void cluster_finalize(const StepParams& p, const Part
             else ((uint16_t*)p.out)[oi] = f32_to_bf16_rne(ov);
         }
         // in-place eviction write (or append): every CTA finished reading K/V before sync #1
-        if (tid < D / 8) {
+        if (sl >= 0 && tid < D / 8) {
             const size_t unit_off = (size_t)u * N * D;
             const uint4* ks = (const uint4*)(p.k_new + (size_t)u * D);
             const uint4* vs = (const uint4*)(p.v_new + (size_t)u * D);

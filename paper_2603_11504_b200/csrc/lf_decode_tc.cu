@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                 for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                if (lane == 0) xs[g] = acc * sl2;
+                if (lane == 0) xs[g] = p.deferred ? -INFINITY : acc * sl2;
             }
             if (sidx == 0) LF_EVENT(ui, 15);
             // ---- max over the unit's logits (TMEM-resident S)
@@ -487,6 +487,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
             if (sidx == 0) LF_EVENT(ui, 12);
             // ---- scores I_j (Eq. 6, mean over the group) from the TMEM logits; local argmin key
             unsigned long long best = ~0ull;
+            const int excl = (p.deferred && p.exclude_newest) ? __ldg(p.written + u) : -1;
             float wM[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
@@ -509,7 +510,8 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
                     const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
                     if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
-                    best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
+                    if (x.c0 + j != excl)
+                        best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
                 }
             }
             ptx::tc_fence_before();
@@ -569,15 +571,20 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
                     unsigned long long mk = ~0ull;
                     for (int r = 0; r < S; ++r)
                         mk = umin64(mk, ptx::ld_dsmem_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key), r)));
-                    const int sl = x.n < N ? x.n : (int)(mk & 0xffffffffull);
-                    *s_slot = sl;
-                    p.slot[u] = sl;
-                    if (x.n < N) p.n_valid[u] = x.n + 1;
+                    if (p.deferred) {        // next step's victim; the current token is already in place
+                        p.pend[u] = (int)(mk & 0xffffffffull);
+                        *s_slot = -1;
+                    } else {
+                        const int sl = x.n < N ? x.n : (int)(mk & 0xffffffffull);
+                        *s_slot = sl;
+                        p.slot[u] = sl;
+                        if (x.n < N) p.n_valid[u] = x.n + 1;
+                    }
                 }
                 ptx::named_bar_sync(1, kNS);
                 const int sl = *s_slot;
                 // every CTA of the cluster consumed unit u's K/V before arriving on kready
-                if (sidx < 16) {
+                if (sl >= 0 && sidx < 16) {
                     const size_t unit_off = (size_t)u * N * 128;
                     ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = kvn[sidx];
                     ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = kvn[16 + sidx];

@@ -19,6 +19,10 @@ struct StepParams {
     int32_t* slot;          // int32 [B][Hkv]
     float* scores;          // fp32 [B][Hkv][N] or nullptr
     unsigned long long* trace;  // debug event trace (LF_TRACE builds only), or nullptr
+    int32_t deferred;       // 1: Fig. 2-literal deferred mode (k*, v* already written; no current-token term)
+    int32_t exclude_newest; // deferred mode: the slot just written is not a candidate
+    int32_t* pend;          // deferred mode: int32 [B][Hkv] slot covered at the next step
+    const int32_t* written; // deferred mode: int32 [B][Hkv] slot the current token was written to
     int32_t B, Hq, Hkv, G, d, N;
     int32_t out_f32;        // 1: fp32 out, 0: bf16 out
     float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip
@@ -34,6 +38,9 @@ struct Plan {
     int32_t clusters; // persistent clusters in the grid (tcgen05 kernel), 0 = one cluster per unit
     int32_t stages;   // TMA ring depth (tcgen05 kernel)
 };
+
+// deferred mode pre-pass: the current token covers pend[u] (or is appended) before attention
+cudaError_t deferred_write_launch(const StepParams& p, cudaStream_t stream);
 
 // CUDA-core split-KV kernel (lf_decode_simt.cu)
 bool simt_supported(int G, int d);

@@ -35,7 +35,7 @@ lf_status cuda_fail(cudaError_t e, const char* what) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    size_t k_off, v_off, nv_off, sq_off, sk_off, sv_off, so_off, ss_off, total;
+    size_t k_off, v_off, nv_off, pd_off, sq_off, sk_off, sv_off, so_off, ss_off, total;
 };
 
 Layout layout_of(const lf_cache_config& c) {
@@ -45,6 +45,7 @@ Layout layout_of(const lf_cache_config& c) {
     L.k_off = off; off = align_up(off + kv, 256);
     L.v_off = off; off = align_up(off + kv, 256);
     L.nv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
+    L.pd_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
     L.sq_off = off; off = align_up(off + (size_t)c.batch * c.num_q_heads * c.head_dim * 2, 256);
     L.sk_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
     L.sv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
@@ -66,7 +67,8 @@ lf_status validate(const lf_cache_config* c) {
     if (c->budget < 2) return fail(LF_ERR_INVALID_ARGUMENT, "budget must be >= 2 (S:123)");
     if (c->out_dtype != LF_DTYPE_BF16 && c->out_dtype != LF_DTYPE_F32)
         return fail(LF_ERR_INVALID_ARGUMENT, "unknown out_dtype %d", c->out_dtype);
-    if (c->mode != LF_EVICT_SAME_STEP) return fail(LF_ERR_UNSUPPORTED, "only same-step mode is built");
+    if (c->mode != LF_EVICT_SAME_STEP && c->mode != LF_EVICT_DEFERRED && c->mode != LF_EVICT_DEFERRED_EXCLUDE_NEWEST)
+        return fail(LF_ERR_INVALID_ARGUMENT, "unknown mode %d", c->mode);
     if (c->kernel < LF_KERNEL_AUTO || c->kernel > LF_KERNEL_TCGEN05)
         return fail(LF_ERR_INVALID_ARGUMENT, "unknown kernel %d", c->kernel);
     if (c->split_tokens < 0 || c->split_tokens % 128)
@@ -87,6 +89,28 @@ __global__ void fill_i32(int32_t* p, int32_t v, int n) {
     if (i < n) p[i] = v;
 }
 
+// Deferred mode pre-pass (Fig. 2 left): one warp per unit.  The current token covers the
+// slot chosen at the previous step when the unit is full, else it is appended at n (R11);
+// slot[u] returns where it went.  A full unit without a pending slot (cannot happen through the
+// API: every step of a full unit sets one) falls back to slot 0.
+__global__ void deferred_write_kernel(lf::StepParams p) {
+    const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (u >= p.B * p.Hkv) return;
+    const int n = p.n_valid[u];
+    int s;
+    if (n < p.N) s = n;
+    else s = p.pend[u] >= 0 && p.pend[u] < p.N ? p.pend[u] : 0;
+    const int rows = p.d / 8;   // uint4 per row
+    const size_t dst = ((size_t)u * p.N + s) * p.d;
+    if (lane < rows) ((uint4*)(p.K + dst))[lane] = ((const uint4*)(p.k_new + (size_t)u * p.d))[lane];
+    else if (lane < 2 * rows) ((uint4*)(p.V + dst))[lane - rows] = ((const uint4*)(p.v_new + (size_t)u * p.d))[lane - rows];
+    if (lane == 0) {
+        p.slot[u] = s;
+        if (n < p.N) p.n_valid[u] = n + 1;
+    }
+}
+
 }  // namespace
 
 struct lf_cache {
@@ -101,6 +125,14 @@ struct lf_cache {
     lf::TcMaps maps;
     unsigned long long* trace;
 };
+
+namespace lf {
+cudaError_t deferred_write_launch(const StepParams& p, cudaStream_t stream) {
+    const int units = p.B * p.Hkv;
+    deferred_write_kernel<<<(units + 7) / 8, 256, 0, stream>>>(p);
+    return cudaGetLastError();
+}
+}  // namespace lf
 
 namespace {
 
@@ -206,8 +238,9 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
         cudaSetDevice(prev);
         return fail(LF_ERR_CUDA, "cuTensorMapEncodeTiled failed for the K/V tensor maps");
     }
-    // all slots invalid; zero-filled storage
+    // all slots invalid; zero-filled storage; no pending victim (-1)
     e = cudaMemset(c->slab, 0, c->L.total);
+    if (e == cudaSuccess) e = cudaMemset((char*)c->slab + c->L.pd_off, 0xff, (size_t)cfg->batch * cfg->num_kv_heads * 4);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -249,7 +282,13 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int
     return LF_OK;
 }
 
-int32_t lf_kernels_per_step(const lf_cache* c) { return c ? 1 : 0; }
+int32_t lf_kernels_per_step(const lf_cache* c) { return c ? (c->cfg.mode == LF_EVICT_SAME_STEP ? 1 : 2) : 0; }
+
+lf_status lf_cache_pending(const lf_cache* c, int32_t** pend) {
+    if (!c || !pend) return fail(LF_ERR_INVALID_ARGUMENT, "cache or pend is NULL");
+    *pend = (int32_t*)((char*)c->slab + c->L.pd_off);
+    return LF_OK;
+}
 
 lf_status lf_debug_set_trace(lf_cache* c, void* device_buf) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
@@ -310,6 +349,10 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.slot = slot;
     p.scores = scores;
     p.trace = c->trace;
+    p.deferred = g.mode != LF_EVICT_SAME_STEP;
+    p.exclude_newest = g.mode == LF_EVICT_DEFERRED_EXCLUDE_NEWEST;
+    p.pend = (int32_t*)(base + c->L.pd_off);
+    p.written = slot;
     p.B = g.batch;
     p.Hq = g.num_q_heads;
     p.Hkv = g.num_kv_heads;
@@ -323,9 +366,11 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);
-    cudaError_t e = c->plan.kernel == LF_KERNEL_TCGEN05
-                        ? lf::tc_launch(p, c->plan, c->maps, (cudaStream_t)stream)
-                        : lf::simt_launch(p, c->plan, (cudaStream_t)stream);
+    cudaError_t e = cudaSuccess;
+    if (p.deferred) e = lf::deferred_write_launch(p, (cudaStream_t)stream);
+    if (e == cudaSuccess)
+        e = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_launch(p, c->plan, c->maps, (cudaStream_t)stream)
+                                                 : lf::simt_launch(p, c->plan, (cudaStream_t)stream);
     if (prev != c->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     return LF_OK;
