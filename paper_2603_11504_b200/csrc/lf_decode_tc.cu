@@ -34,15 +34,13 @@
 namespace lf {
 namespace {
 
-constexpr int kNG = 3;                  // softmax warp groups (4 warps each)
-constexpr int kNT = 64 + 128 * kNG;     // + producer warp + MMA warp
-constexpr int kNS = 128 * kNG;          // softmax threads
+constexpr int kMaxNG = 3;               // softmax warp groups (4 warps each): 3 at one CTA per SM,
+                                        // 1 at two CTAs per SM (register file)
 constexpr int kStageBytes = 32768;      // 128 tokens x 128 d x bf16 (two 16 KB boxes)
 constexpr int kBoxBytes = 16384;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxStages = 6;
 constexpr int kMaxChunk = 4096;         // 2 regions x 32 tiles x 8 columns = 512 TMEM columns
-constexpr uint32_t kTmemCols = 512;
 
 struct TcArgs {
     CUtensorMap tmK;
@@ -50,6 +48,7 @@ struct TcArgs {
     StepParams p;
     int32_t clusters;   // C: persistent clusters in the grid
     int32_t stages;     // ring depth
+    int32_t tmem_cols;  // TMEM columns per CTA (512: one CTA per SM; 256: two)
 };
 
 // exchange buffer, one per unit parity
@@ -64,7 +63,7 @@ struct Xchg {
 struct TcSmem {
     int ring, q, pbuf, L, xb, misc, kvn, red, bars, tmem, total;
 };
-__host__ __device__ inline TcSmem tc_smem(int chunk, int stages) {
+__host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxNG) {
     TcSmem s;
     int off = 0;
     s.ring = off; off += stages * kStageBytes;   // 1024-aligned (swizzle atoms)
@@ -84,8 +83,8 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages) {
 // mbarrier slots
 constexpr int FULL = 0;                 // [kMaxStages]
 constexpr int EMPTY = FULL + kMaxStages;
-constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kNG;
-constexpr int QFULL = PFREE + kNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
+constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kMaxNG;
+constexpr int QFULL = PFREE + kMaxNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
 constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 48, "barrier slots");
@@ -129,14 +128,15 @@ __device__ __forceinline__ UnitInfo unit_info(const StepParams& p, int u, int s)
     return x;
 }
 
-template <int GP>
-__global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
+template <int GP, int kNG>
+__global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
+    constexpr int kNS = 128 * kNG;          // softmax threads
     extern __shared__ unsigned char smem_raw[];
     const StepParams& p = a.p;
     // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int G = p.G, N = p.N, chunk = p.chunk, ST = a.stages;
-    const TcSmem so = tc_smem(chunk, ST);
+    const TcSmem so = tc_smem(chunk, ST, kNG);
     float* Ls = (float*)(smem + so.L);
     Xchg* xb = (Xchg*)(smem + so.xb);
     float* misc = (float*)(smem + so.misc);
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
         ptx::tma_prefetch_desc(&a.tmK);
         ptx::tma_prefetch_desc(&a.tmV);
     }
-    if (warp == 1) ptx::tmem_alloc<kTmemCols>(ptx::smem_u32(smem + so.tmem));
+    if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(smem + so.tmem), (uint32_t)a.tmem_cols);
     if (warp >= 2) {   // zero the Q and P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
         for (int e = tid - 64; e < (2 + kNG) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
@@ -604,13 +604,13 @@ __global__ void __launch_bounds__(kNT, 1) tc_decode_kernel(const __grid_constant
     __syncthreads();
     if (warp == 1) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<kTmemCols>(tmem);
+        ptx::tmem_dealloc(tmem, (uint32_t)a.tmem_cols);
     }
 }
 
 __host__ __device__ constexpr int gpad_tc(int G) { return G <= 4 ? 4 : 8; }
 
-template <int GP>
+template <int GP, int NG>
 cudaError_t set_attrs(int smem, int splits) {
     static int smem_set[64] = {0};
     static bool np_set[64] = {false};
@@ -618,27 +618,27 @@ cudaError_t set_attrs(int smem, int splits) {
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     if (dev >= 64 || smem > smem_set[dev]) {
-        e = cudaFuncSetAttribute(tc_decode_kernel<GP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         if (dev < 64) smem_set[dev] = smem;
     }
     if (splits > 8 && (dev >= 64 || !np_set[dev])) {
-        e = cudaFuncSetAttribute(tc_decode_kernel<GP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         if (dev < 64) np_set[dev] = true;
     }
     return cudaSuccess;
 }
 
-template <int GP>
+template <int GP, int NG>
 int max_active_clusters(int splits, int smem) {
-    if (set_attrs<GP>(smem, splits) != cudaSuccess) {
+    if (set_attrs<GP, NG>(smem, splits) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(splits * 1024, 1, 1);
-    cfg.blockDim = dim3(kNT, 1, 1);
+    cfg.blockDim = dim3(64 + 128 * NG, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -648,20 +648,20 @@ int max_active_clusters(int splits, int smem) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP, NG>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     return n;
 }
 
-template <int GP>
+template <int GP, int NG>
 cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) {
-    cudaError_t e = set_attrs<GP>(plan.smem, plan.splits);
+    cudaError_t e = set_attrs<GP, NG>(plan.smem, plan.splits);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.splits * args.clusters, 1, 1);
-    cfg.blockDim = dim3(kNT, 1, 1);
+    cfg.blockDim = dim3(64 + 128 * NG, 1, 1);
     cfg.dynamicSmemBytes = plan.smem;
     cfg.stream = stream;
     cudaLaunchAttribute attr[1];
@@ -671,7 +671,7 @@ cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP>, args);
+    return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP, NG>, args);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -699,9 +699,9 @@ bool encode_2d(CUtensorMap* m, void* base, uint64_t rows, int d) {
     return r == CUDA_SUCCESS;
 }
 
-int stages_for(int chunk) {
-    const int base = tc_smem(chunk, 0).total;
-    int st = (kSmemLimit - base) / kStageBytes;
+int stages_for(int chunk, int smem_limit, int ng) {
+    const int base = tc_smem(chunk, 0, ng).total;
+    int st = (smem_limit - base) / kStageBytes;
     return st > kMaxStages ? kMaxStages : st;
 }
 
@@ -709,11 +709,13 @@ int stages_for(int chunk) {
 
 bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 
-// Split plan: for each cluster size S in {1, 2, 4, 8, 16} whose chunk (<= 4096 tokens: two TMEM
-// logit regions) leaves room for >= 3 ring stages, the persistent grid holds C_S = cudaOccupancyMaxActiveClusters
-// clusters (capped at the unit count) and needs ceil(units / C_S) rounds of `chunk` tokens per
-// CTA; the plan minimises rounds * (chunk + overhead), the overhead (in streamed tokens) being the
-// measured unit-boundary cost: ~128 tokens alone, ~1024 with the cross-CTA exchange (S > 1).
+// Split plan.  Candidates: cluster size S in {1, 2, 4, 8, 16} (chunk = N/S rounded up to a tile,
+// <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2}: k = 1 takes all 512 TMEM
+// columns and up to 6 ring stages; k = 2 needs chunk <= 1920 (256 columns) and >= 2 stages in
+// 113 KB of SMEM, and lets one CTA's unit-boundary work overlap the other's streaming.  The grid
+// holds C = cudaOccupancyMaxActiveClusters clusters (capped at the unit count); the plan minimises
+// the per-SM time proxy ceil(units / C) * (k * chunk + overhead / k), overhead = the measured
+// unit-boundary cost in streamed tokens (~128 alone, ~1024 with the cross-CTA exchange, S > 1).
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     (void)d;
     (void)num_sms;
@@ -724,6 +726,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     best.smem = 0;
     best.clusters = 0;
     best.stages = 0;
+    best.tmem_cols = 0;
     const int Nr = (N + 127) / 128 * 128;
     long long best_cost = -1;
     for (int S = 1; S <= 16; S *= 2) {
@@ -731,22 +734,40 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         const int splits = (N + chunk - 1) / chunk;
         if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
         if (splits > 16 || chunk > kMaxChunk) continue;
-        const int st = stages_for(chunk);
-        if (st < 3) continue;
-        // >= 120 KB keeps one CTA per SM: each CTA allocates all 512 TMEM columns
-        const int smem = max(tc_smem(chunk, st).total, 120 * 1024);
-        const int C = gpad_tc(G) == 4 ? max_active_clusters<4>(splits, smem) : max_active_clusters<8>(splits, smem);
-        if (C <= 0) continue;
-        const int Cu = C < units ? C : units;
-        const long long rounds = (units + Cu - 1) / Cu;
-        const long long cost = rounds * (chunk + (splits > 1 ? 1024 : 128));   // exchange cost for S > 1
-        if (best_cost < 0 || cost < best_cost) {
-            best_cost = cost;
-            best.splits = splits;
-            best.chunk = chunk;
-            best.smem = smem;
-            best.clusters = Cu;
-            best.stages = st;
+        const int tiles = (chunk + 127) / 128;
+        for (int k = 1; k <= 2; ++k) {
+            int st, smem, cols;
+            const int ng = k == 1 ? kMaxNG : 1;
+            if (k == 1) {
+                st = stages_for(chunk, kSmemLimit, ng);
+                if (st < 3) continue;
+                smem = max(tc_smem(chunk, st, ng).total, 120 * 1024);   // keeps one CTA per SM
+                cols = 512;
+            } else {
+                if (2 * 8 * max(tiles, 2) + 16 > 256) continue;
+                st = stages_for(chunk, 113 * 1024, ng);
+                if (st < 2) continue;
+                smem = tc_smem(chunk, st, ng).total;
+                cols = 256;
+            }
+            const int C = gpad_tc(G) == 4 ? (k == 1 ? max_active_clusters<4, kMaxNG>(splits, smem)
+                                                    : max_active_clusters<4, 1>(splits, smem))
+                                          : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
+                                                    : max_active_clusters<8, 1>(splits, smem));
+            if (C <= 0) continue;
+            const int Cu = C < units ? C : units;
+            const long long rounds = (units + Cu - 1) / Cu;
+            const long long ovh = splits > 1 ? 1024 : 128;
+            const long long cost = rounds * ((long long)k * chunk + ovh / k);
+            if (best_cost < 0 || cost < best_cost) {
+                best_cost = cost;
+                best.splits = splits;
+                best.chunk = chunk;
+                best.smem = smem;
+                best.clusters = Cu;
+                best.stages = st;
+                best.tmem_cols = cols;
+            }
         }
         if (split_tokens > 0) break;
     }
@@ -766,8 +787,10 @@ cudaError_t tc_launch(const StepParams& p, const Plan& plan, const TcMaps& maps,
     args.p = p;
     args.clusters = plan.clusters;
     args.stages = plan.stages;
-    if (gpad_tc(p.G) == 4) return launch_t<4>(args, plan, stream);
-    return launch_t<8>(args, plan, stream);
+    args.tmem_cols = plan.tmem_cols;
+    const bool one = plan.tmem_cols == 512;   // one CTA per SM -> kMaxNG softmax groups
+    if (gpad_tc(p.G) == 4) return one ? launch_t<4, kMaxNG>(args, plan, stream) : launch_t<4, 1>(args, plan, stream);
+    return one ? launch_t<8, kMaxNG>(args, plan, stream) : launch_t<8, 1>(args, plan, stream);
 }
 
 }  // namespace lf

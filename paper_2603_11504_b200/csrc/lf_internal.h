@@ -37,6 +37,7 @@ struct Plan {
     int32_t smem;     // dynamic shared memory bytes per CTA
     int32_t clusters; // persistent clusters in the grid (tcgen05 kernel), 0 = one cluster per unit
     int32_t stages;   // TMA ring depth (tcgen05 kernel)
+    int32_t tmem_cols;  // TMEM columns per CTA (tcgen05 kernel)
 };
 
 // deferred mode pre-pass: the current token covers pend[u] (or is appended) before attention
