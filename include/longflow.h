@@ -130,6 +130,11 @@ lf_status lf_cache_views(const lf_cache* c, void** k, void** v, int32_t** n_vali
 lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
                         int32_t* split_tokens);
 
+/* More of the plan: persistent clusters in the grid (0 = one cluster per unit), TMA ring stages,
+ * TMEM columns per CTA (512 = one CTA per SM, 256 = two, 0 = CUDA-core kernel), SMEM bytes per CTA. */
+lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
+                               int32_t* smem_bytes);
+
 /* Deferred modes: device view of int32 [B][Hkv], the slot the next step's token will cover
  * (-1 = none yet).  In deferred modes lf_decode_step's `slot` returns where the current token
  * was written, and `scores` covers every valid slot including it. */

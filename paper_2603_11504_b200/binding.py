@@ -23,7 +23,7 @@ KERNELS = {"auto": 0, "simt": 1, "tcgen05": 2}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 EXPORTS = ["lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
-           "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_kernels_per_step",
+           "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_cache_plan_detail", "lf_kernels_per_step",
            "lf_debug_set_trace", "lf_cache_pending", "lf_status_string", "lf_last_error"]
 MODES = {"same_step": 0, "deferred": 1, "deferred_exclude_newest": 2}
 
@@ -62,6 +62,8 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_decode_step_host.argtypes = [P, P, P, P, P, P, P]
     lib.lf_cache_views.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
+    lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 4
+    lib.lf_cache_plan_detail.restype = ctypes.c_int
     lib.lf_cache_pending.argtypes = [P, ctypes.POINTER(P)]
     lib.lf_cache_pending.restype = ctypes.c_int
     lib.lf_debug_set_trace.argtypes = [P, P]
@@ -199,7 +201,11 @@ class Cache:
     def plan(self):
         k, s, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _check(load().lf_cache_plan(self._h, ctypes.byref(k), ctypes.byref(s), ctypes.byref(c)), "plan")
-        return dict(kernel=KERNEL_NAMES[k.value], splits=s.value, split_tokens=c.value)
+        cl, st, tc, sm = (ctypes.c_int32() for _ in range(4))
+        _check(load().lf_cache_plan_detail(self._h, ctypes.byref(cl), ctypes.byref(st), ctypes.byref(tc),
+                                           ctypes.byref(sm)), "plan_detail")
+        return dict(kernel=KERNEL_NAMES[k.value], splits=s.value, split_tokens=c.value, clusters=cl.value,
+                    stages=st.value, tmem_cols=tc.value, smem=sm.value)
 
     def set_trace(self, buf):
         """Debug: device buffer for the -DLF_TRACE event trace (None disables)."""

@@ -282,6 +282,16 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int
     return LF_OK;
 }
 
+lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
+                                int32_t* smem_bytes) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (clusters) *clusters = c->plan.clusters;
+    if (stages) *stages = c->plan.stages;
+    if (tmem_cols) *tmem_cols = c->plan.tmem_cols;
+    if (smem_bytes) *smem_bytes = c->plan.smem;
+    return LF_OK;
+}
+
 int32_t lf_kernels_per_step(const lf_cache* c) { return c ? (c->cfg.mode == LF_EVICT_SAME_STEP ? 1 : 2) : 0; }
 
 lf_status lf_cache_pending(const lf_cache* c, int32_t** pend) {

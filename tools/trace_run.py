@@ -22,7 +22,7 @@ del k0, v0
 syn = Synth(wl, device="cuda")
 q, kn, vn = syn.step()
 out, slot, _ = cache.new_outputs()
-ctas = 148 * 2
+ctas = 148 * 4
 tr = torch.zeros(ctas * 64 * 16, dtype=torch.int64, device="cuda")
 for i in range(3):
     cache.decode_step(q, kn, vn, out, slot)
