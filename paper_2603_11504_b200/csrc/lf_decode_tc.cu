@@ -297,6 +297,40 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         const float log2G = log2f((float)G);
         const float invG = 1.0f / (float)G;
         const float sl2 = p.scale_log2;
+        // scores I_j (Eq. 6, mean over the group) of this thread's tokens from the TMEM logits and the
+        // local argmin key (ordered log2 I_j, slot); needs gM, glz of the unit
+        auto unit_scores = [&](const UnitInfo& x, int u, uint32_t sreg) -> unsigned long long {
+            const int nv = x.nv;
+            unsigned long long best = ~0ull;
+            const int excl = (p.deferred && p.exclude_newest) ? __ldg(p.written + u) : -1;
+            float wM[GP];
+#pragma unroll
+            for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
+            for (int t = grp; t < x.ntiles; t += kNG) {
+                uint32_t r[8];
+                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
+                ptx::tmem_ld_wait();
+                const int j = t * 128 + row;
+                if (j < nv) {
+                    const float lam = Ls[j];
+                    float av[GP];
+                    float amax = -INFINITY;
+#pragma unroll
+                    for (int g = 0; g < GP; ++g) {
+                        av[g] = g < G ? __uint_as_float(r[g]) * sl2 - wM[g] : -INFINITY;
+                        amax = fmaxf(amax, av[g]);
+                    }
+                    float ssum = 0.f;
+#pragma unroll
+                    for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
+                    const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
+                    if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
+                    if (x.c0 + j != excl)
+                        best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
+                }
+            }
+            return best;
+        };
         uint32_t it = 0, pi = 0, ui = 0;
         for (int u = cid; u < units; u += C, ++ui) {
             const UnitInfo x = unit_info(p, u, s);
@@ -420,6 +454,83 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int g = 0; g < GP; ++g) red[kNG * 64 + (grp * 4 + q4) * 16 + g] = z[g];
             }
             if (sidx == 0) LF_EVENT(ui, 2);
+            if (S == 1) {
+                // ---- single-CTA unit: M, Z and the output directly, no exchange
+                ptx::named_bar_sync(1, kNS);                                  // red[] complete
+                if (sidx < G) {
+                    const int g = sidx;
+                    float mm = red[g], zz = red[kNG * 64 + g];
+                    for (int w = 1; w < 4 * kNG; ++w) {
+                        mm = fmaxf(mm, red[w * 16 + g]);
+                        zz += red[kNG * 64 + w * 16 + g];
+                    }
+                    const float M = fmaxf(mm, xs[g]);
+                    const float f = ptx::ex2_approx(mm - M);
+                    const float Z = zz * f + ptx::ex2_approx(xs[g] - M);
+                    gM[g] = M;
+                    gZ[g] = Z;
+                    glz[g] = log2f(Z);
+                    misc[80 + g] = f;
+                }
+                ptx::named_bar_sync(1, kNS);
+                if (grp == 0) {   // O^T lane = d: out = (o 2^(m-M) + 2^(x*-M) v*) / Z
+                    ptx::mbar_wait(BAR(OFULL), ui & 1u);
+                    ptx::tc_fence_after();
+                    uint32_t o[16];
+                    if (x.ntiles > 0) {
+                        ptx::tmem_ld_x16(tl + (par ^ 1u) * RC, o);
+                        ptx::tmem_ld_wait();
+                    }
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
+                    const float vv = bf16_to_f32(((const uint16_t*)(smem + so.kvn))[128 + row]);
+#pragma unroll
+                    for (int g = 0; g < GP; ++g) {
+                        if (g < G) {
+                            float acc = x.ntiles > 0 ? (__uint_as_float(o[g]) + __uint_as_float(o[8 + g])) * misc[80 + g] : 0.f;
+                            acc = fmaf(ptx::ex2_approx(xs[g] - gM[g]), vv, acc);
+                            const float ov = acc / gZ[g];
+                            const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + row;
+                            if (p.out_f32) ((float*)p.out)[oi] = ov;
+                            else ((uint16_t*)p.out)[oi] = f32_to_bf16_rne(ov);
+                        }
+                    }
+                }
+                unsigned long long best = unit_scores(x, u, sreg);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(BAR(SFREE + par));
+                if (p.scores)
+                    for (int j = nv + sidx; j < x.c1 - x.c0; j += kNS) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
+                if (lane == 0) kred[warp - 2] = best;
+                ptx::named_bar_sync(1, kNS);
+                if (sidx == 0) {
+                    unsigned long long kb = kred[0];
+                    for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
+                    if (p.deferred) {
+                        p.pend[u] = (int)(kb & 0xffffffffull);
+                        *s_slot = -1;
+                    } else {
+                        const int sl = x.n < N ? x.n : (int)(kb & 0xffffffffull);
+                        *s_slot = sl;
+                        p.slot[u] = sl;
+                        if (x.n < N) p.n_valid[u] = x.n + 1;
+                    }
+                }
+                ptx::named_bar_sync(1, kNS);
+                const int sl = *s_slot;
+                if (sl >= 0 && sidx < 16) {   // in-place eviction write (or append)
+                    const size_t unit_off = (size_t)u * N * 128;
+                    const uint4* kvn4 = (const uint4*)(smem + so.kvn);
+                    ((uint4*)(p.K + unit_off + (size_t)sl * 128))[sidx] = kvn4[sidx];
+                    ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = kvn4[16 + sidx];
+                }
+                ptx::named_bar_sync(1, kNS);   // misc / kvn / red reusable
+                continue;
+            }
             // ---- publish (m, Z, o) in this unit's exchange buffer
             const int xp = ui & 1;
             const uint32_t use = ui >> 1;
@@ -486,34 +597,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::named_bar_sync(1, kNS);
             if (sidx == 0) LF_EVENT(ui, 12);
             // ---- scores I_j (Eq. 6, mean over the group) from the TMEM logits; local argmin key
-            unsigned long long best = ~0ull;
-            const int excl = (p.deferred && p.exclude_newest) ? __ldg(p.written + u) : -1;
-            float wM[GP];
-#pragma unroll
-            for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
-            for (int t = grp; t < x.ntiles; t += kNG) {
-                uint32_t r[8];
-                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::tmem_ld_wait();
-                const int j = t * 128 + row;
-                if (j < nv) {
-                    const float lam = Ls[j];
-                    float av[GP];
-                    float amax = -INFINITY;
-#pragma unroll
-                    for (int g = 0; g < GP; ++g) {
-                        av[g] = g < G ? __uint_as_float(r[g]) * sl2 - wM[g] : -INFINITY;
-                        amax = fmaxf(amax, av[g]);
-                    }
-                    float ssum = 0.f;
-#pragma unroll
-                    for (int g = 0; g < GP; ++g) ssum += ptx::ex2_approx(av[g] - amax);   // 1 <= ssum <= G
-                    const float ls = ptx::lg2_approx(lam * ssum) + amax - log2G;   // log2 I_j, no underflow
-                    if (p.scores) p.scores[(size_t)u * N + x.c0 + j] = lam * ssum * ptx::ex2_approx(amax) * invG;
-                    if (x.c0 + j != excl)
-                        best = umin64(best, ((unsigned long long)ordered_bits(ls) << 32) | (unsigned)(x.c0 + j));
-                }
-            }
+            unsigned long long best = unit_scores(x, u, sreg);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(BAR(SFREE + par));          // S(ui) no longer read
@@ -598,8 +682,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         }
         // drain: no CTA leaves while a peer may still read its exchange buffers
         if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
-        for (uint32_t k = ui >= 2 ? ui - 2 : 0; k < ui; ++k)
-            ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
+        if (S > 1)
+            for (uint32_t k = ui >= 2 ? ui - 2 : 0; k < ui; ++k)
+                ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
     }
     __syncthreads();
     if (warp == 1) {
@@ -712,7 +797,7 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 // Split plan.  Candidates: cluster size S in {1, 2, 4, 8, 16} (chunk = N/S rounded up to a tile,
 // <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2}: k = 1 takes all 512 TMEM
 // columns and up to 6 ring stages; k = 2 needs chunk <= 1920 (256 columns) and >= 2 stages in
-// 113 KB of SMEM, and lets one CTA's unit-boundary work overlap the other's streaming.  The grid
+// 110 KB of SMEM, and lets one CTA's unit-boundary work overlap the other's streaming.  The grid
 // holds C = cudaOccupancyMaxActiveClusters clusters (capped at the unit count); the plan minimises
 // the per-SM time proxy ceil(units / C) * (k * chunk + overhead / k), overhead = the measured
 // unit-boundary cost in streamed tokens (~128 alone, ~1024 with the cross-CTA exchange, S > 1).
@@ -745,7 +830,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                 cols = 512;
             } else {
                 if (2 * 8 * max(tiles, 2) + 16 > 256) continue;
-                st = stages_for(chunk, 113 * 1024, ng);
+                st = stages_for(chunk, 110 * 1024, ng);
                 if (st < 2) continue;
                 smem = tc_smem(chunk, st, ng).total;
                 cols = 256;
