@@ -26,6 +26,8 @@
 //           output combine; rank 0 picks the slot (lowest index on ties) and evicts in place
 //           (Fig. 2); `xfree` arrivals release the exchange buffers.
 #include <cuda.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <cudaTypedefs.h>
 
 #include "lf_common.cuh"
@@ -839,11 +841,14 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                                                     : max_active_clusters<4, 1>(splits, smem))
                                           : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
                                                     : max_active_clusters<8, 1>(splits, smem));
-            if (C <= 0) continue;
             const int Cu = C < units ? C : units;
-            const long long rounds = (units + Cu - 1) / Cu;
+            const long long rounds = Cu > 0 ? (units + Cu - 1) / Cu : 0;
             const long long ovh = splits > 1 ? 1024 : 128;
             const long long cost = rounds * ((long long)k * chunk + ovh / k);
+            if (getenv("LF_DEBUG_PLAN"))
+                fprintf(stderr, "[lf plan] S=%d chunk=%d k=%d stages=%d smem=%d C=%d rounds=%lld cost=%lld\n", splits,
+                        chunk, k, st, smem, C, rounds, cost);
+            if (C <= 0) continue;
             if (best_cost < 0 || cost < best_cost) {
                 best_cost = cost;
                 best.splits = splits;
