@@ -707,6 +707,8 @@ cudaError_t set_attrs(int smem, int splits) {
     if (dev >= 64 || smem > smem_set[dev]) {
         e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e != cudaSuccess) return e;
         if (dev < 64) smem_set[dev] = smem;
     }
     if (splits > 8 && (dev >= 64 || !np_set[dev])) {
@@ -738,6 +740,14 @@ int max_active_clusters(int splits, int smem) {
     if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP, NG>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
+    }
+    if (getenv("LF_DEBUG_PLAN")) {
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tc_decode_kernel<GP, NG>, 64 + 128 * NG, smem);
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, tc_decode_kernel<GP, NG>);
+        fprintf(stderr, "[lf plan] NG=%d smem=%d blocks/SM=%d regs=%d maxdyn=%d clusters=%d\n", NG, smem, b,
+                fa.numRegs, fa.maxDynamicSharedSizeBytes, n);
     }
     return n;
 }
