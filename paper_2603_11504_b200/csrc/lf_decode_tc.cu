@@ -73,7 +73,7 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxN
     s.pbuf = off; off += kNG * 4096;             // P^T operand per group: 16 rows x 128 tokens
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
-    s.misc = off; off += 128 * 4;
+    s.misc = off; off += 512 * 4;                // scalars + per-rank combine factors [16][16]
     s.kvn = off;  off += 2 * 256;                // k_new, v_new rows of the current unit
     s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
     s.bars = off; off += 48 * 8;
@@ -579,22 +579,28 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
             const uint32_t xc_addr = ptx::smem_u32(xc);
-            if (sidx < G) {
-                const int g = sidx;
-                float M = xs[g];
-                for (int r = 0; r < S; ++r)
-                    M = fmaxf(M, ptx::ld_dsmem_f32(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, m) + 4 * g, r)));
-                float Z = 0.f;
-                for (int r = 0; r < S; ++r) {
-                    const uint32_t ra = ptx::mapa(xc_addr, r);
-                    const float mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
-                    const float zr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, z) + 4 * g);
-                    Z += zr * ptx::ex2_approx(mr - M);   // same factors as the P and o combination
+            float* fr = misc + 128;    // [g][r] = 2^(m_g,r - M_g)
+            for (int g = warp - 2; g < G; g += 4 * kNG) {   // one warp per head, lane r <-> rank r
+                float mr = -INFINITY, zr = 0.f;
+                if (lane < S) {
+                    const uint32_t ra = ptx::mapa(xc_addr, lane);
+                    mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
+                    zr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, z) + 4 * g);
                 }
+                float M = fmaxf(xs[g], mr);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                const float f = lane < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
+                float Z = zr * f;
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
                 Z += ptx::ex2_approx(xs[g] - M);
-                gM[g] = M;
-                gZ[g] = Z;
-                glz[g] = log2f(Z);
+                if (lane < S) fr[g * 16 + lane] = f;
+                if (lane == 0) {
+                    gM[g] = M;
+                    gZ[g] = Z;
+                    glz[g] = log2f(Z);
+                }
             }
             ptx::named_bar_sync(1, kNS);
             if (sidx == 0) LF_EVENT(ui, 12);
@@ -618,19 +624,29 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             // ---- output combine, split over the ranks: rank s owns float4 elements [s*E4, (s+1)*E4)
             {
+                // S consecutive lanes share one float4 element: lane r loads rank r's partial
                 const int E4 = (G * 32 + S - 1) / S;
-                const int i4_0 = s * E4, i4_1 = min(G * 32, i4_0 + E4);
+                const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
                 const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
-                for (int i4 = i4_0 + sidx; i4 < i4_1; i4 += kNS) {
+                const int r = lane % S, per_warp = 32 / S;
+                for (int e0 = ((sidx >> 5) * per_warp); e0 < cnt; e0 += (kNS >> 5) * per_warp) {
+                    const int e = e0 + lane / S;
+                    const bool ok = e < cnt;
+                    const int i4 = i4_0 + (ok ? e : 0);
                     const int g = i4 >> 5, l = (i4 & 31) * 4;
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int r = 0; r < S; ++r) {
-                        const uint32_t ra = ptx::mapa(xc_addr, r);
-                        const float f = ptx::ex2_approx(ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g) - gM[g]);
-                        const float4 o4 = ptx::ld_dsmem_f32x4(ra + (uint32_t)offsetof(Xchg, o) + 16 * i4);
-                        acc.x = fmaf(o4.x, f, acc.x); acc.y = fmaf(o4.y, f, acc.y);
-                        acc.z = fmaf(o4.z, f, acc.z); acc.w = fmaf(o4.w, f, acc.w);
+                    if (ok) {
+                        const float f = fr[g * 16 + r];
+                        const float4 o4 = ptx::ld_dsmem_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * i4, r));
+                        acc = make_float4(o4.x * f, o4.y * f, o4.z * f, o4.w * f);
                     }
+                    for (int off = S >> 1; off > 0; off >>= 1) {
+                        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+                        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+                        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+                        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+                    }
+                    if (!ok || r != 0) continue;
                     const float fn = ptx::ex2_approx(xs[g] - gM[g]);
                     const uint2 vw = *(const uint2*)(vn + l);
                     const float invZ = 1.0f / gZ[g];
