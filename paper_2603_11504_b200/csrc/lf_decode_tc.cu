@@ -624,23 +624,24 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             // ---- output combine, split over the ranks: rank s owns float4 elements [s*E4, (s+1)*E4)
             {
-                // S consecutive lanes share one float4 element: lane r loads rank r's partial
+                // SG = pow2 >= S consecutive lanes share one float4 element: lane r < S loads rank r's part
                 const int E4 = (G * 32 + S - 1) / S;
                 const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
                 const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
-                const int r = lane % S, per_warp = 32 / S;
+                const int SG = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16;
+                const int r = lane % SG, per_warp = 32 / SG;
                 for (int e0 = ((sidx >> 5) * per_warp); e0 < cnt; e0 += (kNS >> 5) * per_warp) {
-                    const int e = e0 + lane / S;
+                    const int e = e0 + lane / SG;
                     const bool ok = e < cnt;
                     const int i4 = i4_0 + (ok ? e : 0);
                     const int g = i4 >> 5, l = (i4 & 31) * 4;
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (ok) {
+                    if (ok && r < S) {
                         const float f = fr[g * 16 + r];
                         const float4 o4 = ptx::ld_dsmem_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * i4, r));
                         acc = make_float4(o4.x * f, o4.y * f, o4.z * f, o4.w * f);
                     }
-                    for (int off = S >> 1; off > 0; off >>= 1) {
+                    for (int off = SG >> 1; off > 0; off >>= 1) {
                         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
                         acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
                         acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
