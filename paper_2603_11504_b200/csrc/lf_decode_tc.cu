@@ -572,9 +572,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::named_bar_sync(1, kNS);
             const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) LF_EVENT(ui, 11);
-            if (sidx == 0) {
-                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(xr_local, r));
-            }
+            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(xr_local, sidx));   // lane r -> rank r
             ptx::mbar_wait_cluster(xr_local, use & 1u);
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
@@ -695,9 +693,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             ptx::named_bar_sync(1, kNS);   // this rank's remote reads of unit u are complete
             if (sidx == 0) LF_EVENT(ui, 14);
-            if (sidx == 0) {
-                for (int r = 0; r < S; ++r) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), r));
-            }
+            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));
         }
         // drain: no CTA leaves while a peer may still read its exchange buffers
         if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
