@@ -131,9 +131,10 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
                         int32_t* split_tokens);
 
 /* More of the plan: persistent clusters in the grid (0 = one cluster per unit), TMA ring stages,
- * TMEM columns per CTA (512 = one CTA per SM, 256 = two, 0 = CUDA-core kernel), SMEM bytes per CTA. */
+ * TMEM columns per CTA (512 = one CTA per SM, 256 = two, 0 = CUDA-core kernel), SMEM bytes per CTA,
+ * rounds of whole units per CTA before the units split across the cluster.  NULL outputs are skipped. */
 lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
-                               int32_t* smem_bytes);
+                               int32_t* smem_bytes, int32_t* solo_rounds);
 
 /* Deferred modes: device view of int32 [B][Hkv], the slot the next step's token will cover
  * (-1 = none yet).  In deferred modes lf_decode_step's `slot` returns where the current token

@@ -62,7 +62,7 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_decode_step_host.argtypes = [P, P, P, P, P, P, P]
     lib.lf_cache_views.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
-    lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 4
+    lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 5
     lib.lf_cache_plan_detail.restype = ctypes.c_int
     lib.lf_cache_pending.argtypes = [P, ctypes.POINTER(P)]
     lib.lf_cache_pending.restype = ctypes.c_int
@@ -201,11 +201,11 @@ class Cache:
     def plan(self):
         k, s, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _check(load().lf_cache_plan(self._h, ctypes.byref(k), ctypes.byref(s), ctypes.byref(c)), "plan")
-        cl, st, tc, sm = (ctypes.c_int32() for _ in range(4))
+        cl, st, tc, sm, so = (ctypes.c_int32() for _ in range(5))
         _check(load().lf_cache_plan_detail(self._h, ctypes.byref(cl), ctypes.byref(st), ctypes.byref(tc),
-                                           ctypes.byref(sm)), "plan_detail")
+                                           ctypes.byref(sm), ctypes.byref(so)), "plan_detail")
         return dict(kernel=KERNEL_NAMES[k.value], splits=s.value, split_tokens=c.value, clusters=cl.value,
-                    stages=st.value, tmem_cols=tc.value, smem=sm.value)
+                    stages=st.value, tmem_cols=tc.value, smem=sm.value, solo_rounds=so.value)
 
     def set_trace(self, buf):
         """Debug: device buffer for the -DLF_TRACE event trace (None disables)."""

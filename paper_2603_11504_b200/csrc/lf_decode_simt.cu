@@ -323,6 +323,7 @@ Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     pl.clusters = 0;
     pl.stages = 2;
     pl.tmem_cols = 0;
+    pl.solo_rounds = 0;
     const int GP = gpad(G);
     const int fixed = simt_smem(d, GP, G, 0).total;
     int chunk_max = (kMaxSmem - fixed) / ((G + 1) * 4) / 128 * 128;

@@ -116,18 +116,40 @@ __device__ __forceinline__ float habs_sum8(const uint4& w) {
 
 struct UnitInfo {
     int u, b, h, n, c0, c1, nv, ntiles;
+    bool split, valid;
 };
-__device__ __forceinline__ UnitInfo unit_info(const StepParams& p, int u, int s) {
+// Work item i of CTA s of cluster cid (all roles walk the same list).  `solo_rounds` rounds of
+// whole units, one per CTA with no exchange (P = C*S units per round), then the remaining units
+// split S ways across the cluster: balanced tails without paying the exchange on every unit.
+__device__ __forceinline__ UnitInfo item_info(const StepParams& p, int cid, int s, int C, int i) {
     UnitInfo x;
+    const int S = p.splits, P = C * S;
+    bool split;
+    int u;
+    if (i < p.solo_rounds) {
+        u = i * P + cid * S + s;
+        split = false;
+    } else {
+        u = p.solo_rounds * P + cid + (i - p.solo_rounds) * C;
+        split = S > 1;
+    }
+    x.valid = u < p.B * p.Hkv;
+    if (!x.valid) return x;
     x.u = u;
+    x.split = split;
     x.b = u / p.Hkv;
     x.h = u % p.Hkv;
     x.n = __ldcg(p.n_valid + u);
-    x.c0 = s * p.chunk;
-    x.c1 = min(x.c0 + p.chunk, p.N);
+    x.c0 = split ? s * p.chunk : 0;
+    x.c1 = split ? min(x.c0 + p.chunk, p.N) : p.N;
     x.nv = max(0, min(x.c1, x.n) - x.c0);
     x.ntiles = (x.nv + 127) / 128;
     return x;
+}
+// tokens one CTA may hold for a unit (TMEM regions, lambda buffer)
+__host__ __device__ inline int tc_hold(int N, int chunk, int solo_rounds) {
+    const int Nr = (N + 127) / 128 * 128;
+    return solo_rounds > 0 && Nr > chunk ? Nr : chunk;
 }
 
 template <int GP, int kNG>
@@ -138,7 +160,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int G = p.G, N = p.N, chunk = p.chunk, ST = a.stages;
-    const TcSmem so = tc_smem(chunk, ST, kNG);
+    const int hold = tc_hold(N, chunk, p.solo_rounds);
+    const TcSmem so = tc_smem(hold, ST, kNG);
     float* Ls = (float*)(smem + so.L);
     Xchg* xb = (Xchg*)(smem + so.xb);
     float* misc = (float*)(smem + so.misc);
@@ -150,7 +173,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     auto BAR = [&](int i) { return bars + 8u * (uint32_t)i; };
     // TMEM regions: S of unit parity `par` at column par*RC (8 columns per tile); O^T of unit
     // parity `par` at the first 16 columns of region par^1
-    const int tmax = (chunk + 127) / 128;
+    const int tmax = (hold + 127) / 128;
     const uint32_t RC = 8u * (uint32_t)(tmax > 2 ? tmax : 2);
 
     cg::cluster_group cluster = cg::this_cluster();
@@ -159,7 +182,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     const int s = (int)cluster.block_rank();
     const int cid = blockIdx.x / S;
     const int C = a.clusters;
-    const int units = p.B * p.Hkv;
 
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
@@ -199,8 +221,10 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     if (warp == 0) {
         // ------------------------------ producer -------------------------------------------------
         uint32_t it = 0, qi = 0;
-        for (int u = cid; u < units; u += C, ++qi) {
-            const UnitInfo x = unit_info(p, u, s);
+        for (int i = 0;; ++i, ++qi) {
+            const UnitInfo x = item_info(p, cid, s, C, i);
+            if (!x.valid) break;
+            const int u = x.u;
             const int qb = qi & 1;
             ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
             // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
@@ -235,8 +259,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
             uint32_t it = 0, pi = 0, ui = 0;
-            for (int u = cid; u < units; u += C, ++ui) {
-                const UnitInfo x = unit_info(p, u, s);
+            for (int i = 0;; ++i, ++ui) {
+                const UnitInfo x = item_info(p, cid, s, C, i);
+                if (!x.valid) break;
                 const uint32_t par = ui & 1u;
                 ptx::mbar_wait(BAR(QFULL + par), (ui >> 1) & 1u);
                 ptx::mbar_wait(BAR(SFREE + par), ((ui >> 1) & 1u) ^ 1u);   // unit ui-2 finalised
@@ -333,9 +358,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             return best;
         };
-        uint32_t it = 0, pi = 0, ui = 0;
-        for (int u = cid; u < units; u += C, ++ui) {
-            const UnitInfo x = unit_info(p, u, s);
+        uint32_t it = 0, pi = 0, ui = 0, xi = 0;
+        for (int i = 0;; ++i, ++ui) {
+            const UnitInfo x = item_info(p, cid, s, C, i);
+            if (!x.valid) break;
+            const int u = x.u;
             const int nv = x.nv;
             const uint32_t par = ui & 1u;
             const uint32_t sreg = tl + par * RC;
@@ -456,7 +483,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int g = 0; g < GP; ++g) red[kNG * 64 + (grp * 4 + q4) * 16 + g] = z[g];
             }
             if (sidx == 0) LF_EVENT(ui, 2);
-            if (S == 1) {
+            if (!x.split) {
                 // ---- single-CTA unit: M, Z and the output directly, no exchange
                 ptx::named_bar_sync(1, kNS);                                  // red[] complete
                 if (sidx < G) {
@@ -534,8 +561,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 continue;
             }
             // ---- publish (m, Z, o) in this unit's exchange buffer
-            const int xp = ui & 1;
-            const uint32_t use = ui >> 1;
+            const int xp = xi & 1;
+            const uint32_t use = xi >> 1;
+            ++xi;
             Xchg* xc = xb + xp;
             ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // readers of its last use are done
             if (sidx == 0) LF_EVENT(ui, 8);
@@ -697,9 +725,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         }
         // drain: no CTA leaves while a peer may still read its exchange buffers
         if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
-        if (S > 1)
-            for (uint32_t k = ui >= 2 ? ui - 2 : 0; k < ui; ++k)
-                ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
+        for (uint32_t k = xi >= 2 ? xi - 2 : 0; k < xi; ++k)
+            ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
     }
     __syncthreads();
     if (warp == 1) {
@@ -820,12 +847,14 @@ int stages_for(int chunk, int smem_limit, int ng) {
 bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 
 // Split plan.  Candidates: cluster size S in {1, 2, 4, 8, 16} (chunk = N/S rounded up to a tile,
-// <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2}: k = 1 takes all 512 TMEM
-// columns and up to 6 ring stages; k = 2 needs chunk <= 1920 (256 columns) and >= 2 stages in
-// 110 KB of SMEM, and lets one CTA's unit-boundary work overlap the other's streaming.  The grid
-// holds C = cudaOccupancyMaxActiveClusters clusters (capped at the unit count); the plan minimises
-// the per-SM time proxy ceil(units / C) * (k * chunk + overhead / k), overhead = the measured
-// unit-boundary cost in streamed tokens (~128 alone, ~1024 with the cross-CTA exchange, S > 1).
+// <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2} x (for S > 1 and N <= 4096)
+// with or without solo rounds.  k = 1 takes all 512 TMEM columns and up to 6 ring stages; k = 2
+// needs <= 1920 held tokens (256 columns) and >= 2 stages in 110 KB of SMEM.  The grid holds
+// C = cudaOccupancyMaxActiveClusters clusters; the plan minimises the per-SM time proxy
+//   solo_rounds * (k N + ovh_1 / k) + split_rounds * (k chunk + ovh_S / k)
+// with the measured unit-boundary overheads in streamed tokens (ovh_1 ~ 128 alone, ovh_S ~ 1024
+// with the cross-CTA exchange).  Solo rounds process whole units per CTA (no exchange); the
+// remaining units are split S ways, which balances the tail.
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     (void)d;
     (void)num_sms;
@@ -837,6 +866,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     best.clusters = 0;
     best.stages = 0;
     best.tmem_cols = 0;
+    best.solo_rounds = 0;
     const int Nr = (N + 127) / 128 * 128;
     long long best_cost = -1;
     for (int S = 1; S <= 16; S *= 2) {
@@ -844,42 +874,56 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         const int splits = (N + chunk - 1) / chunk;
         if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
         if (splits > 16 || chunk > kMaxChunk) continue;
-        const int tiles = (chunk + 127) / 128;
         for (int k = 1; k <= 2; ++k) {
-            int st, smem, cols;
-            const int ng = k == 1 ? kMaxNG : 1;
-            if (k == 1) {
-                st = stages_for(chunk, kSmemLimit, ng);
-                if (st < 3) continue;
-                smem = max(tc_smem(chunk, st, ng).total, 120 * 1024);   // keeps one CTA per SM
-                cols = 512;
-            } else {
-                if (2 * 8 * max(tiles, 2) + 16 > 256) continue;
-                st = stages_for(chunk, 110 * 1024, ng);
-                if (st < 2) continue;
-                smem = tc_smem(chunk, st, ng).total;
-                cols = 256;
-            }
-            const int C = gpad_tc(G) == 4 ? (k == 1 ? max_active_clusters<4, kMaxNG>(splits, smem)
-                                                    : max_active_clusters<4, 1>(splits, smem))
-                                          : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
-                                                    : max_active_clusters<8, 1>(splits, smem));
-            const int Cu = C < units ? C : units;
-            const long long rounds = Cu > 0 ? (units + Cu - 1) / Cu : 0;
-            const long long ovh = splits > 1 ? 1024 : 128;
-            const long long cost = rounds * ((long long)k * chunk + ovh / k);
-            if (getenv("LF_DEBUG_PLAN"))
-                fprintf(stderr, "[lf plan] S=%d chunk=%d k=%d stages=%d smem=%d C=%d rounds=%lld cost=%lld\n", splits,
-                        chunk, k, st, smem, C, rounds, cost);
-            if (C <= 0) continue;
-            if (best_cost < 0 || cost < best_cost) {
-                best_cost = cost;
-                best.splits = splits;
-                best.chunk = chunk;
-                best.smem = smem;
-                best.clusters = Cu;
-                best.stages = st;
-                best.tmem_cols = cols;
+            for (int solo = 0; solo <= 1; ++solo) {
+                if (solo && (splits == 1 || Nr > kMaxChunk || split_tokens > 0)) continue;
+                const int hold = solo ? max(Nr, chunk) : chunk;
+                const int tiles = (hold + 127) / 128;
+                const int ng = k == 1 ? kMaxNG : 1;
+                int st, smem, cols;
+                if (k == 1) {
+                    st = stages_for(hold, kSmemLimit, ng);
+                    if (st < 3) continue;
+                    smem = max(tc_smem(hold, st, ng).total, 120 * 1024);   // keeps one CTA per SM
+                    cols = 512;
+                } else {
+                    if (2 * 8 * max(tiles, 2) + 16 > 256) continue;
+                    st = stages_for(hold, 110 * 1024, ng);
+                    if (st < 2) continue;
+                    smem = tc_smem(hold, st, ng).total;
+                    cols = 256;
+                }
+                const int C = gpad_tc(G) == 4 ? (k == 1 ? max_active_clusters<4, kMaxNG>(splits, smem)
+                                                        : max_active_clusters<4, 1>(splits, smem))
+                                              : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
+                                                        : max_active_clusters<8, 1>(splits, smem));
+                if (C <= 0) continue;
+                const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
+                long long cost, R = 0;
+                int Cu;
+                if (solo) {
+                    R = units / ((long long)C * splits);
+                    if (R == 0) continue;
+                    const long long rem = units - R * C * splits;
+                    Cu = C;
+                    cost = R * ((long long)k * Nr + ovh1 / k) + ((rem + C - 1) / C) * ((long long)k * chunk + ovhS / k);
+                } else {
+                    Cu = C < units ? C : units;
+                    cost = ((units + Cu - 1) / Cu) * ((long long)k * chunk + ovhS / k);
+                }
+                if (getenv("LF_DEBUG_PLAN"))
+                    fprintf(stderr, "[lf plan] S=%d chunk=%d k=%d solo=%d stages=%d smem=%d C=%d R=%lld cost=%lld\n",
+                            splits, chunk, k, solo, st, smem, C, R, cost);
+                if (best_cost < 0 || cost < best_cost) {
+                    best_cost = cost;
+                    best.splits = splits;
+                    best.chunk = chunk;
+                    best.smem = smem;
+                    best.clusters = Cu;
+                    best.stages = st;
+                    best.tmem_cols = cols;
+                    best.solo_rounds = (int)R;
+                }
             }
         }
         if (split_tokens > 0) break;

@@ -28,6 +28,7 @@ struct StepParams {
     float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip
     int32_t splits;         // CTAs per unit (= cluster size)
     int32_t chunk;          // tokens per CTA (multiple of 128)
+    int32_t solo_rounds;    // tcgen05 kernel: rounds of whole units per CTA before the split tail
 };
 
 struct Plan {
@@ -38,6 +39,7 @@ struct Plan {
     int32_t clusters; // persistent clusters in the grid (tcgen05 kernel), 0 = one cluster per unit
     int32_t stages;   // TMA ring depth (tcgen05 kernel)
     int32_t tmem_cols;  // TMEM columns per CTA (tcgen05 kernel)
+    int32_t solo_rounds;  // tcgen05: rounds of whole units per CTA before the split tail
 };
 
 // deferred mode pre-pass: the current token covers pend[u] (or is appended) before attention

@@ -283,8 +283,9 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int
 }
 
 lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
-                                int32_t* smem_bytes) {
+                                int32_t* smem_bytes, int32_t* solo_rounds) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (solo_rounds) *solo_rounds = c->plan.solo_rounds;
     if (clusters) *clusters = c->plan.clusters;
     if (stages) *stages = c->plan.stages;
     if (tmem_cols) *tmem_cols = c->plan.tmem_cols;
@@ -373,6 +374,7 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.scale_log2 = (float)((double)g.softmax_scale * 1.4426950408889634);
     p.splits = c->plan.splits;
     p.chunk = c->plan.chunk;
+    p.solo_rounds = c->plan.solo_rounds;
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);

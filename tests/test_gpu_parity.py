@@ -316,3 +316,15 @@ def test_full_size_sampled_units(cuda_lib, tag):
         s = int(slot[b, h])
         assert s == r["slot"] or r["scores"][s] <= (1 + 1e-4) * r["scores"].min() + 1e-30
     print(f"{tag}: {st}")
+
+
+def test_solo_then_split_schedule(cuda_lib):
+    """A plan with whole-unit (solo) rounds followed by a split tail (B=64, 32/8, N=2048 -> 512
+    units over 74 two-CTA clusters): every unit, solo or split, matches the oracle."""
+    wl = Workload("mix", 64, 32, 8, 128, 2048, 2040, 4)
+    cache, orc, syn = setup_pair(wl, nthreads=8)
+    plan = cache.plan()
+    if plan["solo_rounds"] == 0:
+        pytest.skip(f"planner chose no solo rounds here: {plan}")
+    st = run_lockstep(cache, orc, syn, wl.steps)
+    print(plan, st)
