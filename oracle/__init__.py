@@ -52,6 +52,8 @@ def _load():
             lib.lfo_step_apply.restype = i
             lib.lfo_step_deferred.argtypes = [i, i, i, i, i, dbl, P, P, P, P, P, P, P, P, P, P, i, i]
             lib.lfo_step_deferred.restype = i
+            lib.lfo_snapkv_select.argtypes = [i, i, i, i, i, i, dbl, P, P, P, P, P]
+            lib.lfo_snapkv_select.restype = i
             _lib = lib
     return _lib
 
@@ -179,6 +181,25 @@ class OracleCache:
         if r:
             raise OracleError(f"lfo_step_deferred failed: {r}")
         return out, written, self.pend.copy(), scores
+
+
+def snapkv_select(q_obs, K, budget, pool_kernel=7, scale=None):
+    """SnapKV prefill selection for one unit (NEXT-f3; readings R22-R24).
+    q_obs: uint16 [G][w][d] (the last w prompt positions' queries of the group), K: uint16 [n][d].
+    Returns dict(kept int32 [budget] ascending, score [n-w], pooled [n-w])."""
+    lib = _load()
+    q_obs = _u16(q_obs)
+    G, w, d = q_obs.shape
+    K = _u16(K).reshape(-1, d)
+    n = K.shape[0]
+    sc = (1.0 / np.sqrt(d)) if scale is None else float(scale)
+    kept = np.zeros((budget,), np.int32)
+    score = np.zeros((max(n - w, 1),), np.float64)
+    pooled = np.zeros((max(n - w, 1),), np.float64)
+    r = lib.lfo_snapkv_select(G, d, n, w, pool_kernel, budget, sc, _p(q_obs), _p(K), _p(kept), _p(score), _p(pooled))
+    if r < 0:
+        raise OracleError(f"lfo_snapkv_select failed: {r}")
+    return dict(kept=kept, score=score[:n - w], pooled=pooled[:n - w])
 
 
 def bf16_bits_to_f64(a) -> np.ndarray:

@@ -265,3 +265,66 @@ int lfo_step_deferred(int B, int Hq, int Hkv, int d, int N, double scale,
     free(ex);
     return st;
 }
+
+/* ------------------------------------------------------------------------- */
+/* SnapKV prefill compression (NEXT-f3; "first use SnapKV to compress the tokens to the
+ * budget size"; parameters per SPEC S:300-308; readings R22-R24 in DESIGN.md).
+ * One unit (sequence, kv head) with a prompt of n tokens, G query heads and an observation window
+ * of the last w prompt positions:
+ *   1. for each observation query (g, k), k < w, at prompt position p = n - w + k:
+ *        s_j = scale * q_{g,k} . K_j  for j <= p (causal), alpha = softmax over j <= p
+ *   2. score_i = (1/(G w)) sum_{g,k} alpha_{g,k,i}       for prefix tokens i < n - w
+ *   3. pooled_i = max_{|j - i| <= (ks-1)/2, 0 <= j < n-w} score_j   (1-D max pool, 'same')
+ *   4. keep the (budget - w) prefix tokens with the largest pooled score (ties: lower index),
+ *      plus the w window tokens; kept sorted ascending.
+ * q_obs [G][w][d], K [n][d] bf16 bits.  kept [budget] output, score/pooled [n - w] optional.
+ * Returns the number kept (= budget), or -4 on bad arguments (n <= budget, w > budget, ...). */
+int lfo_snapkv_select(int G, int d, int n, int w, int ks, int budget, double scale,
+                      const uint16_t *q_obs, const uint16_t *K, int32_t *kept,
+                      double *score_out, double *pooled_out) {
+    if (n <= budget || w < 1 || w > budget || w > n || ks < 1 || (ks % 2) == 0) return -4;
+    int np = n - w;                  /* prefix tokens (candidates) */
+    double *score = (double *)calloc((size_t)(np > 0 ? np : 1), sizeof(double));
+    double *pooled = (double *)calloc((size_t)(np > 0 ? np : 1), sizeof(double));
+    double *s = (double *)malloc(sizeof(double) * (size_t)n);
+    char *taken = (char *)calloc((size_t)(np > 0 ? np : 1), 1);
+    if (!score || !pooled || !s || !taken) { free(score); free(pooled); free(s); free(taken); return -3; }
+    for (int g = 0; g < G; ++g) {
+        for (int k = 0; k < w; ++k) {
+            const uint16_t *qr = q_obs + ((size_t)g * w + k) * d;
+            int p = n - w + k;
+            double m = 0.0;
+            for (int j = 0; j <= p; ++j) {           /* step 1: causal logits */
+                double dot = 0.0;
+                for (int l = 0; l < d; ++l) dot += bf16_to_f64(qr[l]) * bf16_to_f64(K[(size_t)j * d + l]);
+                s[j] = scale * dot;
+                if (j == 0 || s[j] > m) m = s[j];
+            }
+            double z = 0.0;
+            for (int j = 0; j <= p; ++j) z += exp(s[j] - m);
+            for (int i = 0; i < np; ++i) score[i] += exp(s[i] - m) / z;   /* step 2 (sum) */
+        }
+    }
+    for (int i = 0; i < np; ++i) score[i] /= (double)(G * w);            /* step 2 (mean) */
+    int r = (ks - 1) / 2;
+    for (int i = 0; i < np; ++i) {                                        /* step 3 */
+        double mx = score[i];
+        for (int j = i - r; j <= i + r; ++j)
+            if (j >= 0 && j < np && score[j] > mx) mx = score[j];
+        pooled[i] = mx;
+    }
+    int want = budget - w;                                                /* step 4 */
+    for (int c = 0; c < want; ++c) {
+        int best = -1;
+        for (int i = 0; i < np; ++i)
+            if (!taken[i] && (best < 0 || pooled[i] > pooled[best])) best = i;
+        taken[best] = 1;
+    }
+    int o = 0;
+    for (int i = 0; i < np; ++i) if (taken[i]) kept[o++] = i;
+    for (int k = 0; k < w; ++k) kept[o++] = np + k;
+    if (score_out) memcpy(score_out, score, sizeof(double) * (size_t)np);
+    if (pooled_out) memcpy(pooled_out, pooled, sizeof(double) * (size_t)np);
+    free(score); free(pooled); free(s); free(taken);
+    return o;
+}
