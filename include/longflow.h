@@ -101,6 +101,23 @@ lf_status lf_cache_destroy(lf_cache* c);
 lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v, int32_t n,
                           void* stream);
 
+/* SnapKV prefill compression (NEXT-f3; "if the number of tokens in the prefill stage exceeds
+ * the budget, we first use SnapKV to compress the tokens to the budget size"; readings R22-R24):
+ * per kv head, rows (g, k) = the G query heads x the last w prompt positions attend causally;
+ * score_i = mean attention of prefix token i < n-w; pooled = odd-kernel 1-D max pool ('same');
+ * the (budget - w) largest pooled prefix tokens (ties: lower index) plus the w window tokens, in
+ * ascending order, fill slots [0, budget) of sequence `seq` (n_valid = budget).  n <= budget is a
+ * plain lf_prefill_fill.
+ *   k, v       bf16 [Hkv][n][d] (post-RoPE)      q_obs bf16 [Hq][w][d]: queries of positions n-w..n-1
+ *   kept       int32 [Hkv][budget] or NULL: the kept prompt positions
+ *   workspace  device memory of lf_snapkv_workspace_bytes(c, n, w) bytes (caller-owned)
+ * Limits: n <= 65536, 1 <= w <= min(budget, n), G * w <= 128, pool_kernel odd.  Enqueued on
+ * `stream`. */
+lf_status lf_snapkv_workspace_bytes(const lf_cache* c, int32_t n, int32_t w, size_t* bytes);
+lf_status lf_prefill_snapkv(lf_cache* c, int32_t seq, const void* k, const void* v, const void* q_obs,
+                            int32_t n, int32_t w, int32_t pool_kernel, int32_t* kept, void* workspace,
+                            void* stream);
+
 /* One fused decode step over the whole cache (Alg. 1 + Fig. 2 left, same-step mode R1):
  *   q      bf16 [B][Hq][d]       current token's queries (post-RoPE)
  *   k_new  bf16 [B][Hkv][d]      current token's key   (post-RoPE)

@@ -24,7 +24,7 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 EXPORTS = ["lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
            "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_cache_plan_detail", "lf_kernels_per_step",
-           "lf_debug_set_trace", "lf_cache_pending", "lf_status_string", "lf_last_error"]
+           "lf_debug_set_trace", "lf_cache_pending", "lf_snapkv_workspace_bytes", "lf_prefill_snapkv", "lf_status_string", "lf_last_error"]
 MODES = {"same_step": 0, "deferred": 1, "deferred_exclude_newest": 2}
 
 
@@ -64,6 +64,10 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
     lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 5
     lib.lf_cache_plan_detail.restype = ctypes.c_int
+    lib.lf_snapkv_workspace_bytes.argtypes = [P, i32, i32, ctypes.POINTER(sz)]
+    lib.lf_snapkv_workspace_bytes.restype = ctypes.c_int
+    lib.lf_prefill_snapkv.argtypes = [P, i32, P, P, P, i32, i32, i32, P, P, P]
+    lib.lf_prefill_snapkv.restype = ctypes.c_int
     lib.lf_cache_pending.argtypes = [P, ctypes.POINTER(P)]
     lib.lf_cache_pending.restype = ctypes.c_int
     lib.lf_debug_set_trace.argtypes = [P, P]
@@ -158,6 +162,16 @@ class Cache:
         """k, v: bf16 CUDA tensors [Hkv][n][d]."""
         n = 0 if k is None else int(k.shape[1])
         _check(load().lf_prefill_fill(self._h, seq, _ptr(k), _ptr(v), n, _stream(stream)), "lf_prefill_fill")
+
+    def prefill_snapkv(self, seq, k, v, q_obs, window=32, pool_kernel=7, kept=None, stream=None):
+        """SnapKV-compressed prefill (NEXT-f3): k, v bf16 [Hkv][n][d], q_obs bf16 [Hq][w][d]."""
+        n, w = int(k.shape[1]), int(window)
+        nb = ctypes.c_size_t()
+        _check(load().lf_snapkv_workspace_bytes(self._h, n, w, ctypes.byref(nb)), "lf_snapkv_workspace_bytes")
+        ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
+        _check(load().lf_prefill_snapkv(self._h, seq, _ptr(k), _ptr(v), _ptr(q_obs), n, w, pool_kernel, _ptr(kept),
+                                        ws.data_ptr(), _stream(stream)), "lf_prefill_snapkv")
+        return ws   # keep alive until the stream has run it
 
     def decode_step(self, q, k_new, v_new, out, slot, scores=None, stream=None):
         _check(load().lf_decode_step(self._h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), _ptr(slot),

@@ -45,6 +45,13 @@ struct Plan {
 // deferred mode pre-pass: the current token covers pend[u] (or is appended) before attention
 cudaError_t deferred_write_launch(const StepParams& p, cudaStream_t stream);
 
+// SnapKV prefill compression (lf_snapkv.cu, NEXT-f3)
+constexpr int kSnapRowsMax = 128;
+size_t snapkv_workspace_bytes(int Hkv, int G, int n, int w, int N);
+cudaError_t snapkv_launch(uint16_t* K, uint16_t* V, int32_t* n_valid, int seq, int Hkv, int G, int d, int N,
+                          const void* k, const void* v, const void* q_obs, int n, int w, int ks, float scale,
+                          int32_t* kept, void* workspace, cudaStream_t stream);
+
 // CUDA-core split-KV kernel (lf_decode_simt.cu)
 bool simt_supported(int G, int d);
 Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms);

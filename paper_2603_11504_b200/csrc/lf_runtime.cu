@@ -342,6 +342,50 @@ lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v
     return LF_OK;
 }
 
+static lf_status snapkv_check(const lf_cache* c, int32_t n, int32_t w, int32_t pool_kernel) {
+    const lf_cache_config& g = c->cfg;
+    const int G = g.num_q_heads / g.num_kv_heads;
+    if (n < 1 || n > 65536) return fail(LF_ERR_INVALID_ARGUMENT, "prompt length %d out of [1, 65536]", n);
+    if (w < 1 || w > g.budget || w > n) return fail(LF_ERR_INVALID_ARGUMENT, "window %d must be in [1, min(budget, n)]", w);
+    if ((long long)G * w > lf::kSnapRowsMax)
+        return fail(LF_ERR_UNSUPPORTED, "G * window = %d > %d observation rows", G * w, lf::kSnapRowsMax);
+    if (pool_kernel < 1 || pool_kernel % 2 == 0) return fail(LF_ERR_INVALID_ARGUMENT, "pool kernel must be odd");
+    return LF_OK;
+}
+
+lf_status lf_snapkv_workspace_bytes(const lf_cache* c, int32_t n, int32_t w, size_t* bytes) {
+    if (!c || !bytes) return fail(LF_ERR_INVALID_ARGUMENT, "cache or bytes is NULL");
+    lf_status s = snapkv_check(c, n, w, 1);
+    if (s) return s;
+    const lf_cache_config& g = c->cfg;
+    *bytes = n > g.budget ? lf::snapkv_workspace_bytes(g.num_kv_heads, g.num_q_heads / g.num_kv_heads, n, w, g.budget)
+                          : 0;
+    return LF_OK;
+}
+
+lf_status lf_prefill_snapkv(lf_cache* c, int32_t seq, const void* k, const void* v, const void* q_obs, int32_t n,
+                            int32_t w, int32_t pool_kernel, int32_t* kept, void* workspace, void* stream) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    const lf_cache_config& g = c->cfg;
+    if (seq < 0 || seq >= g.batch) return fail(LF_ERR_INVALID_ARGUMENT, "seq %d of %d", seq, g.batch);
+    lf_status s = snapkv_check(c, n, w, pool_kernel);
+    if (s) return s;
+    if (!k || !v) return fail(LF_ERR_INVALID_ARGUMENT, "k or v is NULL");
+    if (n <= g.budget) return lf_prefill_fill(c, seq, k, v, n, stream);   // nothing to compress
+    if (!q_obs || !workspace) return fail(LF_ERR_INVALID_ARGUMENT, "q_obs and workspace are required when n > budget");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    char* base = (char*)c->slab;
+    cudaError_t e = lf::snapkv_launch((uint16_t*)(base + c->L.k_off), (uint16_t*)(base + c->L.v_off),
+                                      (int32_t*)(base + c->L.nv_off), seq, g.num_kv_heads,
+                                      g.num_q_heads / g.num_kv_heads, g.head_dim, g.budget, k, v, q_obs, n, w,
+                                      pool_kernel, g.softmax_scale, kept, workspace, (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "snapkv");
+    return LF_OK;
+}
+
 lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
                          int32_t* slot, float* scores, void* stream) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
