@@ -131,6 +131,18 @@ lf_status lf_prefill_snapkv(lf_cache* c, int32_t seq, const void* k, const void*
 lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new,
                          void* out, int32_t* slot, float* scores, void* stream);
 
+/* Approximation diagnostics (NEXT-f4; PAPER §3.3, App. A): call BEFORE lf_decode_step with the same
+ * inputs; reads the pre-step cache.  Per unit, the exact eviction objective with the current query
+ * E_i = mean_g ||o_g - o_g^(\i)||^2 (Eq. 3's right-hand side, via the exact remainder P:424-426) is
+ * compared with LongFlowScore (Eq. 6):
+ *   islot int32 [B][Hkv][3]: {LongFlow victim, argmin_i E_i (lowest index on ties), rank of the
+ *                             LongFlow victim under E (0 = the same quality)}  (-1 if n == 0)
+ *   fstat fp32 [B][Hkv][3]:  {E(LongFlow victim), E(exact victim), max_i ||R_i|| / bound (<= 1)}
+ *   workspace: lf_diag_workspace_bytes bytes of device memory.  Plain CUDA-core kernel (not the hot path). */
+lf_status lf_diag_workspace_bytes(const lf_cache* c, size_t* bytes);
+lf_status lf_diagnose_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, int32_t* islot,
+                           float* fstat, void* workspace, void* stream);
+
 /* Same step with HOST buffers (the end-to-end entry point): copies q/k_new/v_new host ->
  * device (pinned host memory recommended), runs lf_decode_step on `stream`, copies out and
  * slot device -> host and synchronises `stream` before returning. Layouts as above. */

@@ -24,7 +24,8 @@ KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 
 EXPORTS = ["lf_cache_bytes", "lf_cache_create", "lf_cache_destroy", "lf_prefill_fill", "lf_decode_step",
            "lf_decode_step_host", "lf_cache_views", "lf_cache_plan", "lf_cache_plan_detail", "lf_kernels_per_step",
-           "lf_debug_set_trace", "lf_cache_pending", "lf_snapkv_workspace_bytes", "lf_prefill_snapkv", "lf_status_string", "lf_last_error"]
+           "lf_debug_set_trace", "lf_cache_pending", "lf_snapkv_workspace_bytes", "lf_prefill_snapkv",
+           "lf_diag_workspace_bytes", "lf_diagnose_step", "lf_status_string", "lf_last_error"]
 MODES = {"same_step": 0, "deferred": 1, "deferred_exclude_newest": 2}
 
 
@@ -68,6 +69,10 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_snapkv_workspace_bytes.restype = ctypes.c_int
     lib.lf_prefill_snapkv.argtypes = [P, i32, P, P, P, i32, i32, i32, P, P, P]
     lib.lf_prefill_snapkv.restype = ctypes.c_int
+    lib.lf_diag_workspace_bytes.argtypes = [P, ctypes.POINTER(sz)]
+    lib.lf_diag_workspace_bytes.restype = ctypes.c_int
+    lib.lf_diagnose_step.argtypes = [P, P, P, P, P, P, P, P]
+    lib.lf_diagnose_step.restype = ctypes.c_int
     lib.lf_cache_pending.argtypes = [P, ctypes.POINTER(P)]
     lib.lf_cache_pending.restype = ctypes.c_int
     lib.lf_debug_set_trace.argtypes = [P, P]
@@ -172,6 +177,18 @@ class Cache:
         _check(load().lf_prefill_snapkv(self._h, seq, _ptr(k), _ptr(v), _ptr(q_obs), n, w, pool_kernel, _ptr(kept),
                                         ws.data_ptr(), _stream(stream)), "lf_prefill_snapkv")
         return ws   # keep alive until the stream has run it
+
+    def diagnose_step(self, q, k_new, v_new, stream=None):
+        """NEXT-f4 diagnostics on the pre-step cache: (islot int32 [B][Hkv][3], fstat fp32 [B][Hkv][3])."""
+        nb = ctypes.c_size_t()
+        _check(load().lf_diag_workspace_bytes(self._h, ctypes.byref(nb)), "lf_diag_workspace_bytes")
+        ws = torch.empty(max(nb.value, 1), dtype=torch.uint8, device=self.device)
+        islot = torch.empty(self.B, self.Hkv, 3, dtype=torch.int32, device=self.device)
+        fstat = torch.empty(self.B, self.Hkv, 3, dtype=torch.float32, device=self.device)
+        _check(load().lf_diagnose_step(self._h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(islot), _ptr(fstat),
+                                       ws.data_ptr(), _stream(stream)), "lf_diagnose_step")
+        self._diag_ws = ws
+        return islot, fstat
 
     def decode_step(self, q, k_new, v_new, out, slot, scores=None, stream=None):
         _check(load().lf_decode_step(self._h, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(out), _ptr(slot),

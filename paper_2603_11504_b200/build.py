@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "liblongflow.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in
-           ("lf_runtime.cu", "lf_decode_simt.cu", "lf_decode_tc.cu", "lf_snapkv.cu")]
+           ("lf_runtime.cu", "lf_decode_simt.cu", "lf_decode_tc.cu", "lf_snapkv.cu", "lf_diag.cu")]
 HEADERS = [os.path.join(HERE, "csrc", f) for f in ("lf_internal.h", "lf_tc_ptx.cuh", "lf_common.cuh")] + [
            os.path.join(ROOT, "include", "longflow.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -52,6 +52,11 @@ cudaError_t snapkv_launch(uint16_t* K, uint16_t* V, int32_t* n_valid, int seq, i
                           const void* k, const void* v, const void* q_obs, int n, int w, int ks, float scale,
                           int32_t* kept, void* workspace, cudaStream_t stream);
 
+// approximation diagnostics (lf_diag.cu, NEXT-f4)
+size_t diag_workspace_bytes(int units, int G, int N);
+cudaError_t diag_launch(const StepParams& p, const int32_t* n_valid, void* workspace, int32_t* islot, float* fstat,
+                        cudaStream_t stream);
+
 // CUDA-core split-KV kernel (lf_decode_simt.cu)
 bool simt_supported(int G, int d);
 Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms);

@@ -386,6 +386,44 @@ lf_status lf_prefill_snapkv(lf_cache* c, int32_t seq, const void* k, const void*
     return LF_OK;
 }
 
+lf_status lf_diag_workspace_bytes(const lf_cache* c, size_t* bytes) {
+    if (!c || !bytes) return fail(LF_ERR_INVALID_ARGUMENT, "cache or bytes is NULL");
+    const lf_cache_config& g = c->cfg;
+    *bytes = lf::diag_workspace_bytes(g.batch * g.num_kv_heads, g.num_q_heads / g.num_kv_heads, g.budget);
+    return LF_OK;
+}
+
+lf_status lf_diagnose_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, int32_t* islot,
+                           float* fstat, void* workspace, void* stream) {
+    if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
+    if (!q || !k_new || !v_new || !islot || !fstat || !workspace)
+        return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new, islot, fstat and workspace must be non-NULL");
+    const lf_cache_config& g = c->cfg;
+    if (g.num_q_heads / g.num_kv_heads > 8) return fail(LF_ERR_UNSUPPORTED, "diagnostics built for G <= 8");
+    char* base = (char*)c->slab;
+    lf::StepParams p = {};
+    p.q = (const uint16_t*)q;
+    p.k_new = (const uint16_t*)k_new;
+    p.v_new = (const uint16_t*)v_new;
+    p.K = (uint16_t*)(base + c->L.k_off);
+    p.V = (uint16_t*)(base + c->L.v_off);
+    p.B = g.batch;
+    p.Hq = g.num_q_heads;
+    p.Hkv = g.num_kv_heads;
+    p.G = g.num_q_heads / g.num_kv_heads;
+    p.d = g.head_dim;
+    p.N = g.budget;
+    p.scale_log2 = (float)((double)g.softmax_scale * 1.4426950408889634);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaError_t e = lf::diag_launch(p, (const int32_t*)(base + c->L.nv_off), workspace, islot, fstat,
+                                    (cudaStream_t)stream);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_fail(e, "diagnose");
+    return LF_OK;
+}
+
 lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
                          int32_t* slot, float* scores, void* stream) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
