@@ -893,10 +893,11 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                     smem = tc_smem(hold, st, ng).total;
                     cols = 256;
                 }
-                const int C = gpad_tc(G) == 4 ? (k == 1 ? max_active_clusters<4, kMaxNG>(splits, smem)
-                                                        : max_active_clusters<4, 1>(splits, smem))
-                                              : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
-                                                        : max_active_clusters<8, 1>(splits, smem));
+                int C = gpad_tc(G) == 4 ? (k == 1 ? max_active_clusters<4, kMaxNG>(splits, smem)
+                                                  : max_active_clusters<4, 1>(splits, smem))
+                                        : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
+                                                  : max_active_clusters<8, 1>(splits, smem));
+                if (k == 2 && getenv("LF_FORCE_K2")) C *= 2;   // experiment: assume 2 CTAs per SM
                 if (C <= 0) continue;
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
                 long long cost, R = 0;
