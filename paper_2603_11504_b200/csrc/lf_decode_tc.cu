@@ -849,7 +849,8 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
 // Split plan.  Candidates: cluster size S in {1, 2, 4, 8, 16} (chunk = N/S rounded up to a tile,
 // <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2} x (for S > 1 and N <= 4096)
 // with or without solo rounds.  k = 1 takes all 512 TMEM columns and up to 6 ring stages; k = 2
-// needs <= 1920 held tokens (256 columns) and >= 2 stages in 110 KB of SMEM.  The grid holds
+// needs <= 1920 held tokens (256 columns) and >= 2 stages in 110 KB of SMEM (one softmax group).
+// The grid holds
 // C = cudaOccupancyMaxActiveClusters clusters; the plan minimises the per-SM time proxy
 //   solo_rounds * (k N + ovh_1 / k) + split_rounds * (k chunk + ovh_S / k)
 // with the measured unit-boundary overheads in streamed tokens (ovh_1 ~ 128 alone, ovh_S ~ 1024
@@ -897,7 +898,11 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                                                   : max_active_clusters<4, 1>(splits, smem))
                                         : (k == 1 ? max_active_clusters<8, kMaxNG>(splits, smem)
                                                   : max_active_clusters<8, 1>(splits, smem));
-                if (k == 2 && getenv("LF_FORCE_K2")) C *= 2;   // experiment: assume 2 CTAs per SM
+                // The occupancy API reports one block per SM for the one-group variant although two
+                // fit (2 x 93 KB SMEM, 2 x 30K registers, 2 x 256 TMEM columns); measured on B200 the
+                // two co-reside (e.g. 512 x N=512: 200 -> 166 us), so the k = 2 grid is doubled.  The
+                // persistent loop is correct either way (no cross-cluster dependency).
+                if (k == 2) C *= 2;
                 if (C <= 0) continue;
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
                 long long cost, R = 0;
