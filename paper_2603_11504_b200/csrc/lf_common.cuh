@@ -32,6 +32,11 @@ __device__ __forceinline__ float lds_f32(const float* p) {
     return v;
 }
 
+// Programmatic dependent launch: let the next kernel in the stream start its prologue now, and wait
+// until the previous kernel's memory is visible before the first dependent global access.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long umin64(unsigned long long a, unsigned long long b) {
     return a < b ? a : b;
 }

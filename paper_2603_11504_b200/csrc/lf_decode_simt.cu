@@ -107,6 +107,8 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
     const int s = (int)cluster.block_rank();
     const int u = blockIdx.x / S;
     const int b = u / p.Hkv, h = u % p.Hkv;
+    pdl_trigger();
+    pdl_wait();   // the previous step's cache writes are visible from here on
     const int n = p.n_valid[u];
     const int c0 = s * chunk;
     const int c1 = min(c0 + chunk, N);
@@ -303,13 +305,9 @@ cudaError_t launch_t(const StepParams& p, const Plan& plan, cudaStream_t stream)
     cfg.blockDim = dim3(kNT, 1, 1);
     cfg.dynamicSmemBytes = plan.smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = plan.splits;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    cfg.numAttrs = fill_launch_attrs(attr, plan.splits);
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, p);
 }
 

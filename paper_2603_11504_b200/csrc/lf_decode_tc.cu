@@ -216,6 +216,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     ptx::tc_fence_before();
     ptx::cluster_sync_all();   // barriers of every rank initialised before any remote arrival
     ptx::tc_fence_after();
+    pdl_trigger();             // the next step's prologue may overlap this step
+    pdl_wait();                // the previous step's cache writes are visible from here on
     const uint32_t tmem = *(volatile uint32_t*)(smem + so.tmem);
 
     if (warp == 0) {
@@ -801,13 +803,9 @@ cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) 
     cfg.blockDim = dim3(64 + 128 * NG, 1, 1);
     cfg.dynamicSmemBytes = plan.smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = plan.splits;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    cfg.numAttrs = fill_launch_attrs(attr, plan.splits);
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP, NG>, args);
 }
 

@@ -31,6 +31,11 @@ struct StepParams {
     int32_t solo_rounds;    // tcgen05 kernel: rounds of whole units per CTA before the split tail
 };
 
+// launch attributes shared by the decode kernels: cluster dims + programmatic dependent launch
+// (the kernels call griddepcontrol.wait before their first dependent global access); LF_NO_PDL=1
+// disables the latter
+int fill_launch_attrs(cudaLaunchAttribute* attr, int cluster_x);
+
 struct Plan {
     int32_t kernel;   // lf_kernel (resolved: SIMT or TCGEN05)
     int32_t splits;

@@ -127,6 +127,18 @@ struct lf_cache {
 };
 
 namespace lf {
+int fill_launch_attrs(cudaLaunchAttribute* attr, int cluster_x) {
+    static const bool no_pdl = getenv("LF_NO_PDL") != nullptr;
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster_x;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    if (no_pdl) return 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    return 2;
+}
+
 cudaError_t deferred_write_launch(const StepParams& p, cudaStream_t stream) {
     const int units = p.B * p.Hkv;
     deferred_write_kernel<<<(units + 7) / 8, 256, 0, stream>>>(p);
