@@ -261,12 +261,20 @@ def main():
         return 2
 
     from paper_2603_11504_b200 import Cache
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; LF_BENCH_SHARE_GPU=1 maps every rank to the visible GPUs round-robin and
+    # uses gloo (functional check of the multi-rank path on a single-GPU box, not a measurement)
+    share = os.environ.get("LF_BENCH_SHARE_GPU") == "1"
+    local_dev = local % torch.cuda.device_count() if share else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    local = local_dev
     pg = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
     cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,

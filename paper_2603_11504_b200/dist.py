@@ -36,6 +36,10 @@ def shard(batch: int, world: int, rank: int, scaling: str = "weak"):
 def gather_rows(t: torch.Tensor) -> torch.Tensor:
     """All-gather equal shards along dim 0 (rank order) -> the full-batch tensor on every rank."""
     world = dist.get_world_size()
+    if dist.get_backend() != "nccl":   # gloo (CPU tests): list form
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t.contiguous())
+        return torch.cat(parts, dim=0)
     out = torch.empty((world * t.shape[0], *t.shape[1:]), dtype=t.dtype, device=t.device)
     dist.all_gather_into_tensor(out, t.contiguous())
     return out
