@@ -124,7 +124,20 @@ struct lf_cache {
     lf::Plan plan;
     lf::TcMaps maps;
     unsigned long long* trace;
+    char* host_stage;      // pinned staging for small lf_decode_step_host calls (one H2D + one D2H)
 };
+
+namespace {
+// lf_decode_step_host packs the inputs (and the outputs) into one transfer each when they are small:
+// a copy costs microseconds of fixed latency, a host memcpy of a few KB almost nothing
+constexpr size_t kPackLimit = 256 * 1024;
+size_t stage_in_bytes(const Layout& L, const lf_cache_config& g) {
+    return L.sv_off + (size_t)g.batch * g.num_kv_heads * g.head_dim * 2 - L.sq_off;
+}
+size_t stage_out_bytes(const Layout& L, const lf_cache_config& g) {
+    return L.ss_off + (size_t)g.batch * g.num_kv_heads * 4 - L.so_off;
+}
+}  // namespace
 
 namespace lf {
 int fill_launch_attrs(cudaLaunchAttribute* attr, int cluster_x) {
@@ -242,6 +255,14 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
         c->owns = true;
     }
     c->slab_bytes = c->L.total;
+    c->host_stage = nullptr;
+    if (stage_in_bytes(c->L, c->cfg) + stage_out_bytes(c->L, c->cfg) <= kPackLimit) {
+        if (cudaHostAlloc((void**)&c->host_stage, stage_in_bytes(c->L, c->cfg) + stage_out_bytes(c->L, c->cfg),
+                          cudaHostAllocDefault) != cudaSuccess) {
+            c->host_stage = nullptr;   // optional: fall back to one copy per tensor
+            cudaGetLastError();
+        }
+    }
     if (c->plan.kernel == LF_KERNEL_TCGEN05 &&
         !lf::tc_make_maps(&c->maps, (char*)c->slab + c->L.k_off, (char*)c->slab + c->L.v_off,
                           (long long)cfg->batch * cfg->num_kv_heads, cfg->budget, cfg->head_dim)) {
@@ -271,6 +292,7 @@ lf_status lf_cache_destroy(lf_cache* c) {
     cudaSetDevice(c->device);
     cudaError_t e = cudaDeviceSynchronize();
     if (c->owns) cudaFree(c->slab);
+    if (c->host_stage) cudaFreeHost(c->host_stage);
     cudaSetDevice(prev);
     delete c;
     if (e != cudaSuccess) return cuda_fail(e, "destroy");
@@ -497,18 +519,38 @@ lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
-    cudaError_t e = cudaMemcpyAsync(base + c->L.sq_off, q_host, qb, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sk_off, k_new_host, kb, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sv_off, v_new_host, kb, cudaMemcpyHostToDevice, st);
+    cudaError_t e;
+    char* hs = c->host_stage;
+    const size_t in_b = stage_in_bytes(c->L, g);
+    if (hs) {   // small step: pack the three inputs, one H2D copy
+        memcpy(hs, q_host, qb);
+        memcpy(hs + (c->L.sk_off - c->L.sq_off), k_new_host, kb);
+        memcpy(hs + (c->L.sv_off - c->L.sq_off), v_new_host, kb);
+        e = cudaMemcpyAsync(base + c->L.sq_off, hs, in_b, cudaMemcpyHostToDevice, st);
+    } else {
+        e = cudaMemcpyAsync(base + c->L.sq_off, q_host, qb, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sk_off, k_new_host, kb, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sv_off, v_new_host, kb, cudaMemcpyHostToDevice, st);
+    }
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "h2d");
     lf_status s = lf_decode_step(c, base + c->L.sq_off, base + c->L.sk_off, base + c->L.sv_off,
                                  base + c->L.so_off, (int32_t*)(base + c->L.ss_off), nullptr, stream);
     if (s) return s;
     cudaSetDevice(c->device);
-    e = cudaMemcpyAsync(out_host, base + c->L.so_off, ob, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(slot_host, base + c->L.ss_off, sb, cudaMemcpyDeviceToHost, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (hs) {   // one D2H copy of out + slot, then unpack
+        char* ho = hs + in_b;
+        e = cudaMemcpyAsync(ho, base + c->L.so_off, stage_out_bytes(c->L, g), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) {
+            memcpy(out_host, ho, ob);
+            memcpy(slot_host, ho + (c->L.ss_off - c->L.so_off), sb);
+        }
+    } else {
+        e = cudaMemcpyAsync(out_host, base + c->L.so_off, ob, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(slot_host, base + c->L.ss_off, sb, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    }
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "d2h");
     return LF_OK;
