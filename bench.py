@@ -219,7 +219,10 @@ def config_of(args, wl, B_total, plan):
          "l2": "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(
              2 * wl.N * wl.d * 2 * wl.Hkv * B_total / max(args.gpus, 1) / 1e9)}
     if plan:
-        c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"]})
+        c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"],
+                  "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1})
+    if getattr(args, "mode", "same_step") != "same_step":
+        c["mode"] = args.mode
     return c
 
 
@@ -239,6 +242,8 @@ def main():
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--split-tokens", type=int, default=0)
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--mode", default="same_step", choices=["same_step", "deferred", "deferred_exclude_newest"],
+                    help="eviction mode (R1); deferred = Fig. 2 literal (NEXT-f1)")
     ap.add_argument("--no-graph", action="store_true", help="launch steps directly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
@@ -278,13 +283,15 @@ def main():
         pg = dist
 
     cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
-                  split_tokens=args.split_tokens, device=local)
+                  split_tokens=args.split_tokens, device=local, mode=args.mode)
     plan = cache.plan()
     K, V, nv = cache.views()
     k0, v0 = random_cache(B, wl.Hkv, wl.N, wl.d, seed=args.seed, device=dev, b0=b0)
     K.copy_(k0)
     V.copy_(v0)
     nv.fill_(wl.N)
+    if args.mode != "same_step":
+        cache.pending().zero_()   # every unit full with a pending victim (slot 0) before the first step
     del k0, v0
     syn = Synth(wl, seed=args.seed, device=dev, B=B, b0=b0)
     pool = [syn.step() for _ in range(8)]
