@@ -166,7 +166,7 @@ lf_status make_plan(lf_cache* c) {
     int G = g.num_q_heads / g.num_kv_heads;
     int units = g.batch * g.num_kv_heads;
     bool want_tc = g.kernel == LF_KERNEL_TCGEN05 ||
-                   (g.kernel == LF_KERNEL_AUTO && G >= 4 && lf::tc_supported(G, g.head_dim));
+                   (g.kernel == LF_KERNEL_AUTO && lf::tc_supported(G, g.head_dim));
     if (want_tc) {
         if (!lf::tc_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "tcgen05 kernel not built for G=%d d=%d", G, g.head_dim);
