@@ -53,17 +53,16 @@ struct TcArgs {
     int32_t tmem_cols;  // TMEM columns per CTA (512: one CTA per SM; 256: two)
 };
 
-// exchange buffer, one per unit parity
+// Exchange INBOX of a CTA, one per unit parity, written by the cluster's senders (push model: every
+// remote access is a store followed by a release-arrive; all reads after the acquire are local)
 struct Xchg {
-    float m[16];
-    float z[16];
-    unsigned long long key;
-    unsigned long long pad;
-    float o[8 * 128];   // [GP][128], un-normalised
+    float mz[16][16][2];          // [sender r][g] = (m_g, Z_g) of rank r
+    unsigned long long key[16];   // [sender r] argmin key of rank r (read by rank 0)
+    float o[8 * 128 + 64];        // [sender r][e]: rank r's un-normalised o over MY output slice
 };
 
 struct TcSmem {
-    int ring, q, pbuf, L, xb, misc, kvn, red, bars, tmem, total;
+    int ring, q, pbuf, L, xb, misc, ostage, kvn, red, bars, tmem, total;
 };
 __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxNG) {
     TcSmem s;
@@ -74,6 +73,7 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxN
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 512 * 4;                // scalars + per-rank combine factors [16][16]
+    s.ostage = off; off += 8 * 128 * 4;          // this CTA's un-normalised o_g (split units)
     s.kvn = off;  off += 2 * 256;                // k_new, v_new rows of the current unit
     s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
     s.bars = off; off += 48 * 8;
@@ -562,12 +562,15 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::named_bar_sync(1, kNS);   // misc / kvn / red reusable
                 continue;
             }
-            // ---- publish (m, Z, o) in this unit's exchange buffer
+            // ---- push (m, Z, o slices) into every rank's inbox for this unit parity
             const int xp = xi & 1;
             const uint32_t use = xi >> 1;
             ++xi;
-            Xchg* xc = xb + xp;
-            ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // readers of its last use are done
+            Xchg* xc = xb + xp;                       // my inbox (the same offset in every rank)
+            const uint32_t xc_addr = ptx::smem_u32(xc);
+            float* ost = (float*)(smem + so.ostage);
+            const int E4 = (G * 32 + S - 1) / S;      // float4 output elements per rank
+            ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // every receiver consumed use-1
             if (sidx == 0) LF_EVENT(ui, 8);
             if (grp == 0) {   // group 0 drains O (TMEM lane = d)
                 ptx::mbar_wait(BAR(OFULL), ui & 1u);
@@ -579,41 +582,45 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::tmem_ld_wait();
 #pragma unroll
                     for (int g = 0; g < GP; ++g)
-                        if (g < G) xc->o[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
+                        if (g < G) ost[g * 128 + row] = __uint_as_float(o[g]) + __uint_as_float(o[8 + g]);
                 } else {
-                    for (int g = 0; g < G; ++g) xc->o[g * 128 + row] = 0.f;
+                    for (int g = 0; g < G; ++g) ost[g * 128 + row] = 0.f;
                 }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(OFREE));
             }
-            ptx::named_bar_sync(1, kNS);                                // red[] and xc->o complete
+            ptx::named_bar_sync(1, kNS);                                // red[] and ost complete
             if (sidx == 0) LF_EVENT(ui, 10);
-            if (sidx < G) {
-                const int g = sidx;
+            if (sidx < S * G) {                                         // (m_g, Z_g) -> rank t
+                const int t = sidx / G, g = sidx % G;
                 float mm = red[g], zz = red[kNG * 64 + g];
                 for (int w = 1; w < 4 * kNG; ++w) {
                     mm = fmaxf(mm, red[w * 16 + g]);
                     zz += red[kNG * 64 + w * 16 + g];
                 }
-                xc->m[g] = mm;
-                xc->z[g] = zz;
+                ptx::st_dsmem_f32x2(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, mz) + 8 * (s * 16 + g), t), mm, zz);
             }
-            ptx::named_bar_sync(1, kNS);
+            for (int e = sidx; e < S * E4; e += kNS) {                  // o slice of rank t -> rank t
+                const int t = e / E4, i4 = t * E4 + e % E4;
+                if (i4 < G * 32) {
+                    const float4 v4 = *(const float4*)(ost + 4 * i4);
+                    ptx::st_dsmem_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * (s * E4 + e % E4), t), v4);
+                }
+            }
+            ptx::named_bar_sync(1, kNS);                                // all pushes issued
             const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) LF_EVENT(ui, 11);
             if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(xr_local, sidx));   // lane r -> rank r
-            ptx::mbar_wait_cluster(xr_local, use & 1u);
+            ptx::mbar_wait_cluster(xr_local, use & 1u);                 // every sender pushed to me
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
-            const uint32_t xc_addr = ptx::smem_u32(xc);
             float* fr = misc + 128;    // [g][r] = 2^(m_g,r - M_g)
             for (int g = warp - 2; g < G; g += 4 * kNG) {   // one warp per head, lane r <-> rank r
                 float mr = -INFINITY, zr = 0.f;
                 if (lane < S) {
-                    const uint32_t ra = ptx::mapa(xc_addr, lane);
-                    mr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, m) + 4 * g);
-                    zr = ptx::ld_dsmem_f32(ra + (uint32_t)offsetof(Xchg, z) + 4 * g);
+                    mr = xc->mz[lane][g][0];
+                    zr = xc->mz[lane][g][1];
                 }
                 float M = fmaxf(xs[g], mr);
 #pragma unroll
@@ -643,17 +650,16 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
             if (lane == 0) kred[warp - 2] = best;
             ptx::named_bar_sync(1, kNS);
-            if (sidx == 0) {
+            if (sidx == 0) {   // key -> rank 0's inbox, then release to rank 0
                 LF_EVENT(ui, 4);
                 unsigned long long kb = kred[0];
                 for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
-                xc->key = kb;
+                ptx::st_dsmem_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key) + 8 * s, 0), kb);
                 ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
             }
-            // ---- output combine, split over the ranks: rank s owns float4 elements [s*E4, (s+1)*E4)
+            // ---- output combine of my slice from the inbox: S consecutive lanes (SG = pow2 >= S)
+            //      share one float4 element, lane r reads sender r's part
             {
-                // SG = pow2 >= S consecutive lanes share one float4 element: lane r < S loads rank r's part
-                const int E4 = (G * 32 + S - 1) / S;
                 const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
                 const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
                 const int SG = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16;
@@ -666,7 +672,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (ok && r < S) {
                         const float f = fr[g * 16 + r];
-                        const float4 o4 = ptx::ld_dsmem_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * i4, r));
+                        const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
                         acc = make_float4(o4.x * f, o4.y * f, o4.z * f, o4.w * f);
                     }
                     for (int off = SG >> 1; off > 0; off >>= 1) {
@@ -700,8 +706,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::mbar_wait_cluster(BAR(KREADY + xp), use & 1u);
                 if (sidx == 0) {
                     unsigned long long mk = ~0ull;
-                    for (int r = 0; r < S; ++r)
-                        mk = umin64(mk, ptx::ld_dsmem_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key), r)));
+                    for (int r = 0; r < S; ++r) mk = umin64(mk, xc->key[r]);
                     if (p.deferred) {        // next step's victim; the current token is already in place
                         p.pend[u] = (int)(mk & 0xffffffffull);
                         *s_slot = -1;
@@ -721,11 +726,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ((uint4*)(p.V + unit_off + (size_t)sl * 128))[sidx] = kvn[16 + sidx];
                 }
             }
-            ptx::named_bar_sync(1, kNS);   // this rank's remote reads of unit u are complete
+            ptx::named_bar_sync(1, kNS);   // my inbox of unit u is consumed
             if (sidx == 0) LF_EVENT(ui, 14);
-            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));
+            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));   // senders may reuse it
         }
-        // drain: no CTA leaves while a peer may still read its exchange buffers
+        // drain: no CTA leaves before every peer released (consumed) the inboxes it pushed to
         if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
         for (uint32_t k = xi >= 2 ? xi - 2 : 0; k < xi; ++k)
             ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
