@@ -10,7 +10,9 @@ A "step" is one lf_decode_step over every (sequence, kv head) unit of the rank's
 hot path (logits, softmax, PV, LongFlowScore, argmin, in-place eviction) on a FULL static cache,
 so every step evicts.  value = tokens/s summed over ranks (one token per sequence per step).
 Inputs of 8 pre-generated steps live in HBM; the cache (8.6 GB per GPU for `r`) is far larger
-than L2, so no L2 flush is needed between steps.
+than L2, so no L2 flush is needed between steps.  Caches below FLUSH_BELOW bytes per GPU (`tiny`, `q7`,
+small sweep points) would sit in the 126 MB L2 across steps: there every timed step is preceded by an
+untimed 512 MB write (L2 flush) and bracketed by its own CUDA events; ms_per_step is their mean.
 """
 from __future__ import annotations
 
@@ -211,13 +213,47 @@ def run_reference(args, wl, B_total):
     return 0
 
 
+FLUSH_BELOW = 512 << 20   # cache bytes per GPU under which steps are timed one by one after an L2 flush
+
+
+def cache_bytes_per_gpu(wl, B):
+    return 2 * wl.N * wl.d * 2 * wl.Hkv * B
+
+
+def l2_note(cb):
+    if cb >= FLUSH_BELOW:
+        return "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(cb / 1e9)
+    return ("L2 flushed before every timed step (512 MB write, untimed; cache {:.1f} MB per GPU); "
+            "per-step CUDA events, no graph".format(cb / 1e6))
+
+
+def timed_steps(fn, steps, stream, flush):
+    """ms per step of fn(i) on `stream`: one event pair around all steps, or (flush is a buffer)
+    an untimed L2 flush before every step and per-step event pairs, summed."""
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn(None)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for i in range(steps):
+            flush.add_(1)          # 512 MB read-modify-write: evicts the cache from L2
+            evs[i][0].record(stream)
+            fn(i)
+            evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    return sum(a.elapsed_time(b) for a, b in evs) / steps
+
+
 def config_of(args, wl, B_total, plan):
     c = {"workload": wl.tag, "global_batch": B_total, "batch_per_gpu": B_total // max(args.gpus, 1),
          "num_q_heads": wl.Hq, "num_kv_heads": wl.Hkv, "head_dim": wl.d, "budget": wl.N,
          "cache": "full (every step evicts)", "out_dtype": args.out_dtype,
          "parallelism": f"dp{args.gpus} by sequence (no collective on the hot path)",
-         "l2": "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(
-             2 * wl.N * wl.d * 2 * wl.Hkv * B_total / max(args.gpus, 1) / 1e9)}
+         "l2": l2_note(cache_bytes_per_gpu(wl, B_total // max(args.gpus, 1)))}
     if plan:
         c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"],
                   "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1})
@@ -307,8 +343,11 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
+    flush = None
+    if cache_bytes_per_gpu(wl, B) < FLUSH_BELOW:
+        flush = torch.zeros(128 << 20, dtype=torch.float32, device=dev)
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and flush is None:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             for i in range(args.steps):
@@ -317,23 +356,23 @@ def main():
         graph.replay()     # one untimed replay (graph upload)
         torch.cuda.synchronize(dev)
 
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        if graph is not None:
+    def run_all(i):
+        if i is not None:
+            step(i)
+        elif graph is not None:
             with torch.cuda.stream(stream):
                 graph.replay()
         else:
-            for i in range(args.steps):
-                step(i)
-        ev1.record(stream)
-        torch.cuda.synchronize(dev)
+            for j in range(args.steps):
+                step(j)
+
+    with ClockSampler(local) as clk:
+        ms = timed_steps(run_all, args.steps, stream, flush) * args.steps
     if pg:
         pg.barrier()
-    ms = ev0.elapsed_time(ev1)
     ms_max = lfd.max_over_ranks(ms, device=dev)
     gather = None
     if pg:
@@ -362,13 +401,11 @@ def main():
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        cache.decode_step_host(*hq, oh, sh, stream=stream)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
-    e_ms = torch.tensor([lfd.max_over_ranks(e0.elapsed_time(e1) / e2e_steps, device=dev)])
+    def e2e_run(i):
+        for _ in range(1 if i is not None else e2e_steps):
+            cache.decode_step_host(*hq, oh, sh, stream=stream)
+
+    e_ms = torch.tensor([lfd.max_over_ranks(timed_steps(e2e_run, e2e_steps, stream, flush), device=dev)])
     h2d = sum(t.numel() * t.element_size() for t in hq)
     d2h = oh.numel() * oh.element_size() + sh.numel() * 4
     e2e = {"value": B_total / (float(e_ms.item()) / 1e3), "unit": "tokens/s",

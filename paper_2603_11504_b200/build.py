@@ -36,6 +36,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(out: str, defines=()) -> str:
+    """Debug builds (e.g. -DLF_TRACE) to a separate path, loaded with LF_LIB=<out>."""
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", out, *SOURCES]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stderr[-6000:]}")
+    return out
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)
     print(LIB)

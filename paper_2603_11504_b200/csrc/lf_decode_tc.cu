@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::mbar_init(BAR(QFREE + i), 1);
             ptx::mbar_init(BAR(KDONE + i), 1);
             ptx::mbar_init(BAR(SFREE + i), 4 * kNG);
-            ptx::mbar_init(BAR(XREADY + i), S);    // one arrival per rank
-            ptx::mbar_init(BAR(KREADY + i), S);
+            ptx::mbar_init(BAR(XREADY + i), 1);    // own expect_tx; the senders' st.async complete_tx
+            ptx::mbar_init(BAR(KREADY + i), 1);
             ptx::mbar_init(BAR(XFREE + i), S);
         }
         ptx::mbar_init(BAR(OFULL), 1);
@@ -451,6 +451,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const uint32_t iv = it + x.ntiles + t;
                 const int st = iv % ST;
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
+                if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 5);
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
 #pragma unroll
@@ -570,6 +571,12 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             const uint32_t xc_addr = ptx::smem_u32(xc);
             float* ost = (float*)(smem + so.ostage);
             const int E4 = (G * 32 + S - 1) / S;      // float4 output elements per rank
+            const int my_cnt = max(0, min(G * 32, (s + 1) * E4) - s * E4);
+            if (sidx == 0) {   // bytes every sender pushes into this inbox (phase use-1 already consumed)
+                ptx::mbar_arrive_expect_tx(BAR(XREADY + xp), (uint32_t)(S * (G * 8 + my_cnt * 16)));
+                if (s == 0) ptx::mbar_arrive_expect_tx(BAR(KREADY + xp), (uint32_t)(S * 8));
+            }
+            const uint32_t xr_local = BAR(XREADY + xp);
             ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // every receiver consumed use-1
             if (sidx == 0) LF_EVENT(ui, 8);
             if (grp == 0) {   // group 0 drains O (TMEM lane = d)
@@ -599,20 +606,19 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     mm = fmaxf(mm, red[w * 16 + g]);
                     zz += red[kNG * 64 + w * 16 + g];
                 }
-                ptx::st_dsmem_f32x2(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, mz) + 8 * (s * 16 + g), t), mm, zz);
+                ptx::st_async_f32x2(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, mz) + 8 * (s * 16 + g), t), mm, zz,
+                                    ptx::mapa(xr_local, t));
             }
             for (int e = sidx; e < S * E4; e += kNS) {                  // o slice of rank t -> rank t
                 const int t = e / E4, i4 = t * E4 + e % E4;
                 if (i4 < G * 32) {
                     const float4 v4 = *(const float4*)(ost + 4 * i4);
-                    ptx::st_dsmem_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * (s * E4 + e % E4), t), v4);
+                    ptx::st_async_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * (s * E4 + e % E4), t), v4,
+                                        ptx::mapa(xr_local, t));
                 }
             }
-            ptx::named_bar_sync(1, kNS);                                // all pushes issued
-            const uint32_t xr_local = BAR(XREADY + xp);
             if (sidx == 0) LF_EVENT(ui, 11);
-            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(xr_local, sidx));   // lane r -> rank r
-            ptx::mbar_wait_cluster(xr_local, use & 1u);                 // every sender pushed to me
+            ptx::mbar_wait_cluster(xr_local, use & 1u);                 // every sender's bytes landed
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
             float* fr = misc + 128;    // [g][r] = 2^(m_g,r - M_g)
@@ -654,8 +660,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 LF_EVENT(ui, 4);
                 unsigned long long kb = kred[0];
                 for (int w = 1; w < 4 * kNG; ++w) kb = umin64(kb, kred[w]);
-                ptx::st_dsmem_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key) + 8 * s, 0), kb);
-                ptx::mbar_arrive_remote(ptx::mapa(BAR(KREADY + xp), 0));
+                ptx::st_async_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key) + 8 * s, 0), kb,
+                                  ptx::mapa(BAR(KREADY + xp), 0));
             }
             // ---- output combine of my slice from the inbox: S consecutive lanes (SG = pow2 >= S)
             //      share one float4 element, lane r reads sender r's part
@@ -731,7 +737,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));   // senders may reuse it
         }
         // drain: no CTA leaves before every peer released (consumed) the inboxes it pushed to
-        if (sidx == 0 && ui > 0) LF_EVENT(ui - 1, 5);
         for (uint32_t k = xi >= 2 ? xi - 2 : 0; k < xi; ++k)
             ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
     }

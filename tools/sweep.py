@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from bench import alg_bytes_per_step, peaks
+from bench import FLUSH_BELOW, alg_bytes_per_step, cache_bytes_per_gpu, l2_note, peaks, timed_steps
 from lf_synth import Synth, random_cache, sweep_workload
 from paper_2603_11504_b200 import Cache
 
@@ -36,24 +36,27 @@ for N in map(int, args.budgets.split(",")):
         for i in range(5):
             cache.decode_step(*pool[i % 4], out, slot, stream=st)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=st):
-            for i in range(args.steps):
-                cache.decode_step(*pool[i % 4], out, slot, stream=st)
-        g.replay(); torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(st)
-        with torch.cuda.stream(st):
-            g.replay()
-        e1.record(st)
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / args.steps
+        flush = g = None
+        if cache_bytes_per_gpu(wl, B) < FLUSH_BELOW:   # L2-resident cache: flush before every step
+            flush = torch.zeros(128 << 20, dtype=torch.float32, device="cuda")
+            run = lambda i: cache.decode_step(*pool[i % 4], out, slot, stream=st)
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for i in range(args.steps):
+                    cache.decode_step(*pool[i % 4], out, slot, stream=st)
+            g.replay(); torch.cuda.synchronize()
+
+            def run(i):
+                with torch.cuda.stream(st):
+                    g.replay()
+        us = timed_steps(run, args.steps, st, flush) * 1e3
         alg = alg_bytes_per_step(wl, B, 2)
         rec = {"B": B, "N": N, "latency_us": us, "tokens_per_s": B / (us * 1e-6), "alg_bytes": alg,
                "GBps": alg / (us * 1e-6) / 1e9, "frac_measured_peak": alg / (us * 1e-6) / 1e9 / peak,
-               "plan": cache.plan()}
+               "plan": cache.plan(), "l2": l2_note(cache_bytes_per_gpu(wl, B))}
         print(json.dumps(rec), flush=True)
         f.write(json.dumps(rec) + "\n")
         cache.close()
-        del cache, K, V, nv, pool, out, slot, g
+        del cache, K, V, nv, pool, out, slot, flush, g
         torch.cuda.empty_cache()

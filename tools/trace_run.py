@@ -34,30 +34,35 @@ np.save(f"gpurun_out/trace_{w}.npy", a)
 used = a[:, :, 0] > 0
 t0 = a[used][:, 0].min()
 print("plan", plan, "ctas with events", int(used.any(axis=1).sum()))
-names = ["start", "maxdone", "Vdone", "xready", "scores", "fin", "prodQ", "mmaQ", "xfree", "ofull",
-         "obar", "mz", "MZ", "comb", "r0done", "xsdone"]
+names = ["start", "maxdone", "Vdone", "xready", "keypush", "fin", "prodQ", "mmaQ", "xfree", "ofull",
+         "ostage", "pushed", "MZ", "comb", "r0done", "xsdone"]
 rows = a[used].astype(np.float64)
-for i, j in [(0, 15), (15, 1), (1, 2), (2, 8), (8, 9), (9, 10), (10, 11), (11, 3), (3, 12), (12, 4), (4, 13), (13, 14)]:
+for i, j in [(6, 7), (6, 0), (0, 15), (15, 1), (1, 2), (2, 8), (8, 9), (9, 10), (10, 11), (11, 3), (3, 12),
+             (12, 4), (4, 13), (13, 14)]:
     ok = (rows[:, j] > 0) & (rows[:, i] > 0)
     d = rows[ok, j] - rows[ok, i]
     if not ok.any():
         continue
     print(f"{names[i]}->{names[j]}: mean {d.mean()/1e3:.2f} us  p50 {np.median(d)/1e3:.2f}  max {d.max()/1e3:.2f}")
-# unit-to-unit gap: next unit start - this unit xready/scores
+# absolute timeline of the first unit of every CTA (us from the earliest event)
+first = a[:, 0].astype(np.float64)
+fu = first[(first[:, 6] > 0)]
+tmin = fu[fu > 0].min()
+print("first unit, us after the earliest event (min / mean / max over CTAs):")
+for j in [6, 7, 0, 15, 1, 2, 8, 9, 10, 11, 3, 12, 4, 13, 14]:
+    v = fu[fu[:, j] > 0, j] - tmin
+    if len(v):
+        print(f"  {names[j]:8s} {v.min()/1e3:6.2f} {v.mean()/1e3:6.2f} {v.max()/1e3:6.2f}")
+last = np.array([r[r > 0].max() for r in a[used].astype(np.float64)])
+print(f"kernel event span {(last.max() - tmin)/1e3:.2f} us")
 per_cta = []
 for c in range(ctas):
     u = np.nonzero(used[c])[0]
     if len(u) < 2:
         continue
-    ev = a[c, u].astype(np.float64)
-    per_cta.append(ev)
-    if c < 3:
-        print("cta", c, "units", len(u))
-        for k in range(min(len(u), 4)):
-            print("   ", " ".join(f"{names[i]}={ (ev[k, i]-t0)/1e3:.2f}" for i in range(16) if ev[k, i] > 0))
-gaps = np.concatenate([ev[1:, 0] - ev[:-1, 14] for ev in per_cta])
-print(f"r0done(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
-unit = np.concatenate([ev[1:, 0] - ev[:-1, 0] for ev in per_cta])
-print(f"unit period: mean {unit.mean()/1e3:.2f} us  p50 {np.median(unit)/1e3:.2f}")
-ends = np.array([ev[-1, 4] for ev in per_cta])
-print(f"kernel span {(ends.max()-t0)/1e3:.1f} us; last-unit end spread {(ends.max()-ends.min())/1e3:.1f} us; first start spread {(a[used][:,0].max()-t0)/1e3:.1f}")
+    per_cta.append(a[c, u].astype(np.float64))
+if per_cta:
+    gaps = np.concatenate([ev[1:, 0] - ev[:-1, 14] for ev in per_cta])
+    print(f"r0done(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
+    unit = np.concatenate([ev[1:, 0] - ev[:-1, 0] for ev in per_cta])
+    print(f"unit period: mean {unit.mean()/1e3:.2f} us  p50 {np.median(unit)/1e3:.2f}")
