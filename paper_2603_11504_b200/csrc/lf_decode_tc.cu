@@ -91,14 +91,14 @@ constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
 constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 48, "barrier slots");
 
-// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][16] u64.
+// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][32] u64.
 #ifdef LF_TRACE
 #define LF_EVENT(ui_, slot_)                                                                   \
     do {                                                                                       \
         if (p.trace) {                                                                         \
             unsigned long long t_;                                                             \
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
-            p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 16 + (slot_)] = t_;             \
+            p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 32 + (slot_)] = t_;             \
         }                                                                                      \
     } while (0)
 #else
@@ -106,6 +106,12 @@ static_assert(NBARS <= 48, "barrier slots");
     do {                     \
     } while (0)
 #endif
+// per-tile events of the first units (debug): K tile t landed (MMA warp) in row ui+32, P of V tile t
+// ready in row ui+33 (t < 32)
+#define LF_TILE_EVENT(ui_, row_, t_)            \
+    do {                                        \
+        if ((t_) < 32) LF_EVENT((ui_) + (row_), (t_)); \
+    } while (0)
 
 __device__ __forceinline__ float habs_sum8(const uint4& w) {
     return (fabsf(__uint_as_float(w.x << 16)) + fabsf(__uint_as_float(w.x & 0xffff0000u))) +
@@ -121,7 +127,7 @@ struct UnitInfo {
 // Work item i of CTA s of cluster cid (all roles walk the same list).  `solo_rounds` rounds of
 // whole units, one per CTA with no exchange (P = C*S units per round), then the remaining units
 // split S ways across the cluster: balanced tails without paying the exchange on every unit.
-__device__ __forceinline__ UnitInfo item_info(const StepParams& p, int cid, int s, int C, int i) {
+__device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int s, int C, int i) {
     UnitInfo x;
     const int S = p.splits, P = C * S;
     bool split;
@@ -139,9 +145,15 @@ __device__ __forceinline__ UnitInfo item_info(const StepParams& p, int cid, int 
     x.split = split;
     x.b = u / p.Hkv;
     x.h = u % p.Hkv;
-    x.n = __ldcg(p.n_valid + u);
     x.c0 = split ? s * p.chunk : 0;
     x.c1 = split ? min(x.c0 + p.chunk, p.N) : p.N;
+    return x;
+}
+// ... plus the unit's fill state (read after the PDL wait: the previous step may have appended)
+__device__ __forceinline__ UnitInfo item_info(const StepParams& p, int cid, int s, int C, int i) {
+    UnitInfo x = item_base(p, cid, s, C, i);
+    if (!x.valid) return x;
+    x.n = __ldcg(p.n_valid + x.u);
     x.nv = max(0, min(x.c1, x.n) - x.c0);
     x.ntiles = (x.nv + 127) / 128;
     return x;
@@ -208,6 +220,25 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         ptx::tma_prefetch_desc(&a.tmV);
     }
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(smem + so.tmem), (uint32_t)a.tmem_cols);
+    if (tid == 0) LF_EVENT(0, 16);
+    if (tid == 64) {   // L2 warm-up of the first item's operands; safe before the PDL wait (L2 is coherent)
+        const UnitInfo x = item_base(p, cid, s, C, 0);
+        if (x.valid) {
+            const int u = x.u;
+            ptx::bulk_prefetch_l2(p.n_valid + (u & ~3), 16);
+            ptx::bulk_prefetch_l2(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128, (uint32_t)G * 256);
+            ptx::bulk_prefetch_l2(p.k_new + (size_t)u * 128, 256);
+            ptx::bulk_prefetch_l2(p.v_new + (size_t)u * 128, 256);
+            const int nt = min((x.c1 - x.c0 + 127) / 128, 4);
+            for (int t = 0; t < nt; ++t) {
+                const int row = u * N + x.c0 + t * 128;
+                ptx::tma_prefetch_l2_2d(&a.tmK, 0, row);
+                ptx::tma_prefetch_l2_2d(&a.tmK, 64, row);
+                ptx::tma_prefetch_l2_2d(&a.tmV, 0, row);
+                ptx::tma_prefetch_l2_2d(&a.tmV, 64, row);
+            }
+        }
+    }
     if (warp >= 2) {   // zero the Q and P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
         for (int e = tid - 64; e < (2 + kNG) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
@@ -216,8 +247,10 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     ptx::tc_fence_before();
     ptx::cluster_sync_all();   // barriers of every rank initialised before any remote arrival
     ptx::tc_fence_after();
+    if (tid == 0) LF_EVENT(0, 17);
     pdl_trigger();             // the next step's prologue may overlap this step
     pdl_wait();                // the previous step's cache writes are visible from here on
+    if (tid == 0) LF_EVENT(0, 18);
     const uint32_t tmem = *(volatile uint32_t*)(smem + so.tmem);
 
     if (warp == 0) {
@@ -228,6 +261,23 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (!x.valid) break;
             const int u = x.u;
             const int qb = qi & 1;
+            // the first ring stages go out before Q is staged (they do not depend on it)
+            const int pre = min(2 * x.ntiles, ST);
+            auto issue = [&](int i) {
+                const int st = it % ST;
+                ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
+                const int tile = i < x.ntiles ? i : i - x.ntiles;
+                const int row = u * N + x.c0 + tile * 128;
+                const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
+                const uint32_t dst = ring + (uint32_t)st * kStageBytes;
+                LF_TILE_EVENT(qi, 34, i);
+                ptx::tma_load_2d(dst, tm, BAR(FULL + st), 0, row);
+                ptx::tma_load_2d(dst + kBoxBytes, tm, BAR(FULL + st), 64, row);
+                ++it;
+            };
+            if (lane == 0)
+                for (int i = 0; i < pre; ++i) issue(i);
             ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
             // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
             const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
@@ -241,17 +291,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (lane == 0) {
                 LF_EVENT(qi, 6);
                 ptx::mbar_arrive(BAR(QFULL + qb));
-                for (int i = 0; i < 2 * x.ntiles; ++i, ++it) {
-                    const int st = it % ST;
-                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
-                    ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
-                    const int tile = i < x.ntiles ? i : i - x.ntiles;
-                    const int row = u * N + x.c0 + tile * 128;
-                    const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
-                    const uint32_t dst = ring + (uint32_t)st * kStageBytes;
-                    ptx::tma_load_2d(dst, tm, BAR(FULL + st), 0, row);
-                    ptx::tma_load_2d(dst + kBoxBytes, tm, BAR(FULL + st), 64, row);
-                }
+                for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
             }
             it = __shfl_sync(0xffffffffu, it, 0);
         }
@@ -275,6 +315,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it) {                  // S^T = K_tile . Q^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                    LF_TILE_EVENT(ui, 32, t);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
 #pragma unroll
@@ -473,6 +514,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
+                if (lane == 0 && q4 == 0) LF_TILE_EVENT(ui, 33, t);
             }
             pi += x.ntiles;
             it += 2 * x.ntiles;

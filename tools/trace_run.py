@@ -13,7 +13,8 @@ from paper_2603_11504_b200 import Cache
 
 w = sys.argv[1] if len(sys.argv) > 1 else "r"
 wl = workload_of(w)
-cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype="bf16")
+split = int(sys.argv[sys.argv.index("--split") + 1]) if "--split" in sys.argv else 0
+cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype="bf16", split_tokens=split)
 plan = cache.plan()
 K, V, nv = cache.views()
 k0, v0 = random_cache(wl.B, wl.Hkv, wl.N, wl.d, device="cuda")
@@ -23,19 +24,22 @@ syn = Synth(wl, device="cuda")
 q, kn, vn = syn.step()
 out, slot, _ = cache.new_outputs()
 ctas = 148 * 4
-tr = torch.zeros(ctas * 64 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(ctas * 64 * 32, dtype=torch.int64, device="cuda")
 for i in range(3):
     cache.decode_step(q, kn, vn, out, slot)
 cache.set_trace(tr)
+if "--flush" in sys.argv:   # cold L2 / TLB, as bench.py times L2-resident configs
+    fl = torch.zeros(128 << 20, dtype=torch.float32, device="cuda")
+    fl.amax()
 cache.decode_step(q, kn, vn, out, slot)
 torch.cuda.synchronize()
-a = tr.view(ctas, 64, 16).cpu().numpy().astype(np.int64)
+a = tr.view(ctas, 64, 32).cpu().numpy().astype(np.int64)
 np.save(f"gpurun_out/trace_{w}.npy", a)
 used = a[:, :, 0] > 0
 t0 = a[used][:, 0].min()
 print("plan", plan, "ctas with events", int(used.any(axis=1).sum()))
 names = ["start", "maxdone", "Vdone", "xready", "keypush", "fin", "prodQ", "mmaQ", "xfree", "ofull",
-         "ostage", "pushed", "MZ", "comb", "r0done", "xsdone"]
+         "ostage", "pushed", "MZ", "comb", "r0done", "xsdone", "Vland", "entry", "csync", "pdlw"] + [""] * 12
 rows = a[used].astype(np.float64)
 for i, j in [(6, 7), (6, 0), (0, 15), (15, 1), (1, 2), (2, 8), (8, 9), (9, 10), (10, 11), (11, 3), (3, 12),
              (12, 4), (4, 13), (13, 14)]:
@@ -47,9 +51,11 @@ for i, j in [(6, 7), (6, 0), (0, 15), (15, 1), (1, 2), (2, 8), (8, 9), (9, 10), 
 # absolute timeline of the first unit of every CTA (us from the earliest event)
 first = a[:, 0].astype(np.float64)
 fu = first[(first[:, 6] > 0)]
+fu[:, 16] = first[(first[:, 6] > 0), 5]  # V landed (slot 5)
+fu[:, 17:20] = first[(first[:, 6] > 0), 16:19]
 tmin = fu[fu > 0].min()
 print("first unit, us after the earliest event (min / mean / max over CTAs):")
-for j in [6, 7, 0, 15, 1, 2, 8, 9, 10, 11, 3, 12, 4, 13, 14]:
+for j in [17, 18, 19, 6, 7, 0, 15, 1, 16, 2, 8, 9, 10, 11, 3, 12, 4, 13, 14]:
     v = fu[fu[:, j] > 0, j] - tmin
     if len(v):
         print(f"  {names[j]:8s} {v.min()/1e3:6.2f} {v.mean()/1e3:6.2f} {v.max()/1e3:6.2f}")
