@@ -32,30 +32,33 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-// try_wait with a suspend-time hint: the waiting thread sleeps in hardware until the phase completes
-// (or the hint expires) instead of re-polling.  Measured on B200 (tools/probes/tma_probe2.cu): a
-// polling waiter halves the rate at which TMA fills the SMEM ring of the same SM (32 KB stages:
-// 524 cycles per stage polling vs 261 suspended).
-constexpr uint32_t kSuspendHintNs = 1000000u;
-__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(kSuspendHintNs)
-        : "memory");
-    return ok != 0;
-}
-// Bounded wait: a protocol bug traps (error surfaces at the caller's next sync) instead of
-// hanging the GPU.  The bound (~2^34 cycles, several seconds) is never reached by a live pipeline.
+// Waits.  The product build spins in ONE asm loop {try_wait; @!p bra} -- measured on B200
+// (tools/probes/tma_probe2.cu, 32 KB TMA ring, one SM): this exact loop lets TMA fill the ring at
+// 259 cycles per stage, while any extra instruction in the loop (an iteration bound, a clock read,
+// a suspend-time hint that adds NANOSLEEP.SYNCS) halves the fill rate (518-527 cycles per stage).
+// -DLF_BOUNDED_WAITS (debug / protocol-development builds) traps after ~2^28 retries instead of
+// hanging the GPU on a protocol bug.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    if (mbar_try_wait_sleep(bar, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try_wait_sleep(bar, parity)) {
-        if (clock64() - t0 > (1ll << 34)) __trap();
-    }
+#ifdef LF_BOUNDED_WAITS
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
+        "LF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra.uni LF_DONE;\n\t"
+        "add.u32 n, n, 1;\n\t"
+        "setp.lt.u32 p, n, 0x10000000;\n\t"
+        "@p bra.uni LF_WAIT;\n\t"
+        "trap;\n"
+        "LF_DONE:\n\t}" ::"r"(bar), "r"(parity)
+        : "memory");
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra.uni LF_WAIT;\n\t}" ::"r"(bar), "r"(parity)
+        : "memory");
+#endif
 }
 
 // cluster-scope variants (DSMEM exchange between the CTAs of a cluster)
@@ -67,23 +70,27 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {   // l
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {   // acquire.cluster
+#ifdef LF_BOUNDED_WAITS
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2, %3;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity), "r"(kSuspendHintNs)
+        "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
+        "LF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra.uni LF_DONE;\n\t"
+        "add.u32 n, n, 1;\n\t"
+        "setp.lt.u32 p, n, 0x10000000;\n\t"
+        "@p bra.uni LF_WAIT;\n\t"
+        "trap;\n"
+        "LF_DONE:\n\t}" ::"r"(bar), "r"(parity)
         : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-    if (mbar_try_wait_cluster(bar, parity)) return;
-    const long long t0 = clock64();
-    while (!mbar_try_wait_cluster(bar, parity)) {
-        if (clock64() - t0 > (1ll << 34)) __trap();
-    }
+#else
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "LF_WAIT:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra.uni LF_WAIT;\n\t}" ::"r"(bar), "r"(parity)
+        : "memory");
+#endif
 }
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
 __device__ __forceinline__ float ld_dsmem_f32(uint32_t cluster_addr) {

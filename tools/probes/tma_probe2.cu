@@ -53,6 +53,42 @@ __device__ __forceinline__ void wait_v(uint32_t bar, uint32_t parity) {
                 : "r"(bar), "r"(parity), "r"(1000000u)
                 : "memory");
         }
+    } else if (kW == 4) {   // hinted try_wait loop bounded by an iteration count (no clock reads)
+        uint32_t n = 0;
+        for (;;) {
+            uint32_t ok;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(bar), "r"(parity), "r"(1000000u)
+                : "memory");
+            if (ok) break;
+            if (++n > (1u << 24)) __trap();
+        }
+    } else if (kW == 6) {   // loop inside one asm block, bounded by an iteration count
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
+            "LF_WAIT:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@p bra.uni LF_DONE;\n\t"
+            "add.u32 n, n, 1;\n\t"
+            "setp.lt.u32 p, n, 0x10000000;\n\t"
+            "@p bra.uni LF_WAIT;\n\t"
+            "trap;\n"
+            "LF_DONE:\n\t}" ::"r"(bar), "r"(parity)
+            : "memory");
+    } else if (kW == 7) {   // loop inside one asm block, unbounded
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "LF_WAIT:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra.uni LF_WAIT;\n\t}" ::"r"(bar), "r"(parity)
+            : "memory");
+    } else if (kW == 5) {   // plain try_wait loop (no hint, no bound)
+        while (!ptx::mbar_try_wait(bar, parity)) {
+        }
     } else {                // test_wait spin (never suspends)
         uint32_t ok = 0;
         while (!ok) {
@@ -99,6 +135,68 @@ __global__ void probe_b(const unsigned char* g, int S, int stage_bytes, int iter
     }
 }
 
+// (C) ring whose consumer is the QK MMA of the decode kernel: 8 x tcgen05.mma M128 N8 K16 per 32 KB
+// stage (A = the landed tile, SW128 K-major), tcgen05.commit -> EMPTY.  kMma = 0: consumer arrives
+// without MMA (control).
+template <int kMma>
+__global__ void __launch_bounds__(128, 1) probe_c(const unsigned char* g, int S, int iters, int region, long long* out) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int sb = 32768;
+    const uint32_t ring = ptx::smem_u32(smem), qb = ring + S * sb, full = qb + 4096, empty = full + 8 * S,
+                   tslot = empty + 8 * S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) {
+            ptx::mbar_init(full + 8 * i, 1);
+            ptx::mbar_init(empty + 8 * i, 1);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc(tslot, 32);
+    for (int i = threadIdx.x; i < 1024; i += 128) ((uint32_t*)(smem + S * sb))[i] = 0;
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *(volatile uint32_t*)(smem + (tslot - ring));
+    const long long t0 = clock64();
+    if (threadIdx.x == 0) {
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % S;
+            ptx::mbar_wait(empty + 8 * st, ((it / S) & 1) ^ 1);
+            ptx::mbar_arrive_expect_tx(full + 8 * st, sb);
+            bulk_load_1d(ring + st * sb, g + (size_t)(it * sb % region), sb, full + 8 * st);
+        }
+    } else if (threadIdx.x == 32) {
+        constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 8, 0, 0);
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % S;
+            ptx::mbar_wait(full + 8 * st, (it / S) & 1);
+            if (it < 64) out[it] = clock64() - t0;
+            if (kMma) {
+                ptx::tc_fence_after();
+                const uint32_t base = ring + st * sb;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const uint64_t da = ptx::smem_desc_sw128(base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
+                    const uint64_t db = ptx::smem_desc_sw128(qb + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 1024);
+                    ptx::mma_bf16(tmem + 8u * (it & 3), da, db, idesc, kk > 0);
+                }
+                ptx::mma_commit(empty + 8 * st);
+            } else {
+                ptx::mbar_arrive(empty + 8 * st);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem, 32);
+    }
+}
+
 int main() {
     unsigned char* g;
     cudaMalloc(&g, 64 << 20);
@@ -132,8 +230,8 @@ int main() {
         printf("\n");
     }
     cudaMalloc(&d, 64 * 8);
-    for (int w = 0; w < 4; ++w) {
-        auto k = w == 0 ? probe_b<0> : w == 1 ? probe_b<1> : w == 2 ? probe_b<2> : probe_b<3>;
+    for (int w = 0; w < 8; ++w) {
+        auto k = w == 0 ? probe_b<0> : w == 1 ? probe_b<1> : w == 2 ? probe_b<2> : w == 3 ? probe_b<3> : w == 4 ? probe_b<4> : w == 5 ? probe_b<5> : w == 6 ? probe_b<6> : probe_b<7>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         for (int S : {2, 4, 6}) {
             const int sb = 32768, region = 8 << 20;
@@ -144,10 +242,23 @@ int main() {
             long long h[64];
             cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
             printf("ring wait=%s S=%d: cycles per stage over 8..63: %.0f; first 6:",
-                   w == 0 ? "try_wait" : w == 1 ? "nanosleep" : w == 2 ? "try_wait+hint" : "test_wait", S,
+                   w == 0 ? "mbar_wait" : w == 1 ? "nanosleep" : w == 2 ? "try_wait+hint" : w == 3 ? "test_wait" : w == 4 ? "hint+count" : w == 5 ? "try_wait" : w == 6 ? "asm-loop+bound" : "asm-loop", S,
                    (h[63] - h[7]) / 56.0);
             for (int i = 0; i < 6; ++i) printf(" %lld", h[i]);
             printf("\n");
+        }
+    }
+    for (int m = 0; m < 2; ++m) {
+        auto k = m ? probe_c<1> : probe_c<0>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        for (int S : {2, 4, 6}) {
+            for (int rep = 0; rep < 2; ++rep) {
+                k<<<1, 128, S * 32768 + 4096 + 2048>>>(g, S, 64, 8 << 20, d);
+                cudaDeviceSynchronize();
+            }
+            long long h[64];
+            cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
+            printf("ring+%s S=%d: cycles per stage over 8..63: %.0f\n", m ? "QK-MMA" : "no-MMA", S, (h[63] - h[7]) / 56.0);
         }
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
