@@ -12,7 +12,7 @@ so every step evicts.  value = tokens/s summed over ranks (one token per sequenc
 Inputs of 8 pre-generated steps live in HBM; the cache (8.6 GB per GPU for `r`) is far larger
 than L2, so no L2 flush is needed between steps.  Caches below FLUSH_BELOW bytes per GPU (`tiny`, `q7`,
 small sweep points) would sit in the 126 MB L2 across steps: there every timed step is preceded by an
-untimed 512 MB write (L2 flush) and bracketed by its own CUDA events; ms_per_step is their mean.
+untimed 512 MB read (L2 flush) and bracketed by its own CUDA events; ms_per_step is their mean.
 """
 from __future__ import annotations
 
@@ -223,7 +223,7 @@ def cache_bytes_per_gpu(wl, B):
 def l2_note(cb):
     if cb >= FLUSH_BELOW:
         return "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(cb / 1e9)
-    return ("L2 flushed before every timed step (512 MB write, untimed; cache {:.1f} MB per GPU); "
+    return ("L2 flushed before every timed step (512 MB read, untimed; cache {:.1f} MB per GPU); "
             "per-step CUDA events, no graph".format(cb / 1e6))
 
 
@@ -238,9 +238,12 @@ def timed_steps(fn, steps, stream, flush):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    sink = torch.empty((), dtype=flush.dtype, device=flush.device)
     with torch.cuda.stream(stream):
         for i in range(steps):
-            flush.add_(1)          # 512 MB read-modify-write: evicts the cache from L2
+            # 512 MB READ: evicts the cache from L2 and leaves only clean lines (a write-based flush
+            # would leave ~126 MB of dirty lines whose write-back the timed step would pay for)
+            torch.amax(flush, dim=0, out=sink)
             evs[i][0].record(stream)
             fn(i)
             evs[i][1].record(stream)
