@@ -1,7 +1,8 @@
 """NEXT-f3 measurement: SnapKV prefill compression latency per sequence (all kv heads).
-Work: 2 passes of R x n x d fp32 MACs (R = G * w observation rows) on the CUDA cores + the K/V reads
-and the gather.  The roofline reported is the fp32 FMA peak of the CUDA cores:
-148 SMs x 128 FMA/clk x 2 flop x 1.965 GHz = 74.4 TFLOP/s (B200_PROFILING.md clocks, SM counts).
+Work: 2 passes of R x n x d bf16 MACs (R = G * w observation rows) on the tensor cores (tcgen05) + the
+K reads and the gather.  Rooflines reported: the measured dense bf16 tensor peak (MEASURED_PEAKS.json
+bf16_tflops, burst) for the flops, and the HBM copy peak for the bytes (K read twice + kept K/V rows
+read and written); at these sizes the step is latency-bound (6 launches, 2 of them one CTA per head).
 usage: python tools/bench_snapkv.py [--out gpurun_out/snapkv_bench.jsonl]"""
 import argparse
 import json
@@ -13,7 +14,9 @@ import torch
 
 from paper_2603_11504_b200 import Cache
 
-PEAK_FP32 = 148 * 128 * 2 * 1.965e9
+_pk = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))
+PEAK_BF16 = float(_pk["bf16_tflops"]) * 1e12
+PEAK_HBM = float(_pk["hbm_gbs"]) * 1e9
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default="gpurun_out/snapkv_bench.jsonl")
@@ -37,8 +40,10 @@ for (Hkv, G, n, N, w) in [(8, 4, 8192, 2048, 32), (8, 4, 32768, 3200, 32), (4, 7
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     flops = 2 * 2.0 * Hkv * G * w * n * d
+    byts = 2 * Hkv * n * d * 2 + 2 * 2 * Hkv * N * d * 2
     rec = {"Hkv": Hkv, "G": G, "n": n, "budget": N, "window": w, "us": us, "TFLOPs": flops / (us * 1e-6) / 1e12,
-           "frac_fp32_fma_peak": flops / (us * 1e-6) / PEAK_FP32, "bound": "alu"}
+           "frac_bf16_tensor_peak": flops / (us * 1e-6) / PEAK_BF16, "GBps": byts / (us * 1e-6) / 1e9,
+           "frac_hbm_peak": byts / (us * 1e-6) / PEAK_HBM, "bound": "latency (tensor/hbm fractions both small)"}
     print(json.dumps(rec), flush=True)
     f.write(json.dumps(rec) + "\n")
     del cache, k, v, q, ws
