@@ -75,6 +75,18 @@ def test_random_shapes(cuda_lib, kernel, shape):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
+def test_maximum_budget(cuda_lib, kernel):
+    """The largest budget the library builds (65,536 slots, lf_cache_create's limit): full cache,
+    lockstep eviction steps (tcgen05 G=4: 16 CTAs x 4,096 tokens per unit; CUDA-core G=1)."""
+    Hq = 8 if kernel == "tcgen05" else 2     # the group sizes LF_KERNEL_AUTO routes to each kernel
+    _need(kernel, Hq // 2, 128)
+    wl = Workload("maxN", 1, Hq, 2, 128, 65536, 65536, 3)
+    cache, orc, syn = setup_pair(wl, kernel=kernel, seed=65536)
+    st = run_lockstep(cache, orc, syn, wl.steps)
+    assert st.evictions == 2 * wl.steps and st.max_out_err < 1e-4, st
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_tiling_invariance(cuda_lib, kernel):
     """C.3 #15: results do not depend on the split plan (within fp32), and the
     slot is identical unless the oracle sees a near-tie."""
