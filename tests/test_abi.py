@@ -68,3 +68,21 @@ def test_create_without_gpu_is_a_status_not_a_crash():
     h = ctypes.c_void_p()
     st = binding.load().lf_cache_create(ctypes.byref(cfg), 0, None, 0, ctypes.byref(h))
     assert st in (1, 5) and not h.value
+
+
+def test_missing_extension_fails_loudly():
+    """No CPU fallback: with the CUDA library absent, the product path raises."""
+    import subprocess
+    import sys
+    env = dict(os.environ, LF_LIB="/nonexistent/liblongflow.so")
+    r = subprocess.run([sys.executable, "-c", "from paper_2603_11504_b200 import Cache; Cache(1, 4, 1, 128, 256)"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0 and "not built" in r.stderr, r.stderr[-2000:]
+
+
+@pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_device_fails_loudly():
+    """Without a CUDA device the C ABI reports an error status; nothing computes on the CPU."""
+    from paper_2603_11504_b200 import Cache, LFError
+    with pytest.raises((LFError, RuntimeError)):
+        Cache(1, 4, 1, 128, 256)
