@@ -63,7 +63,7 @@ typedef enum {
 } lf_evict_mode;
 
 typedef enum {
-    LF_KERNEL_AUTO = 0,     /* tcgen05 path when built for (G in [2, 8], d = 128), else the CUDA-core path */
+    LF_KERNEL_AUTO = 0,     /* tcgen05 path when built for (G in [1, 8], d = 128), else the CUDA-core path */
     LF_KERNEL_SIMT = 1,     /* CUDA-core split-KV kernel (G <= 8, d in {64, 128}) */
     LF_KERNEL_TCGEN05 = 2   /* TMA + tcgen05 (TMEM) split-KV kernel, 2 <= G <= 8 */
 } lf_kernel;

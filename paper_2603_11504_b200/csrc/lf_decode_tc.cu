@@ -895,7 +895,7 @@ int stages_for(int chunk, int smem_limit, int ng) {
 
 }  // namespace
 
-bool tc_supported(int G, int d) { return d == 128 && G >= 2 && G <= 8; }
+bool tc_supported(int G, int d) { return d == 128 && G >= 1 && G <= 8; }
 
 // Split plan.  Candidates: cluster size S in {1, 2, 4, 8, 16} (chunk = N/S rounded up to a tile,
 // <= 4096 so two TMEM logit regions fit) x k CTAs per SM in {1, 2} x (for S > 1 and N <= 4096)

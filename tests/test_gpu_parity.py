@@ -60,6 +60,8 @@ SHAPES = [  # (B, Hq, Hkv, d, N, prefill, steps, split_tokens)
     (1, 2, 1, 128, 700, 650, 60, 0),    # G=2 crossing the fill boundary
     (64, 32, 8, 128, 384, 380, 6, 0),   # 512 units: several units per persistent cluster
     (48, 32, 8, 128, 384, 370, 14, 128),  # 384 units x 3-CTA clusters, fill -> evict
+    (2, 3, 3, 128, 300, 290, 14, 128),  # G=1 at d=128 (tcgen05 with one live head), 3 splits
+    (5, 4, 4, 128, 640, 630, 14, 0),    # G=1, solo units
 ]
 
 

@@ -14,11 +14,14 @@ from paper_2603_11504_b200 import Cache
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default="gpurun_out/gsweep.jsonl")
+ap.add_argument("--only-g", type=int, default=0, help="restrict to one group size")
 args = ap.parse_args()
 peak, _ = peaks()
 f = open(args.out, "w")
-for (G, d, kernel) in [(1, 128, "simt"), (1, 64, "simt"), (2, 128, "auto"), (2, 128, "simt"), (4, 128, "auto"),
-                       (4, 128, "simt"), (7, 128, "auto"), (8, 128, "auto"), (8, 64, "simt")]:
+for (G, d, kernel) in [(1, 128, "auto"), (1, 128, "simt"), (1, 64, "simt"), (2, 128, "auto"), (2, 128, "simt"),
+                       (4, 128, "auto"), (4, 128, "simt"), (7, 128, "auto"), (8, 128, "auto"), (8, 64, "simt")]:
+    if args.only_g and G != args.only_g:
+        continue
     B, Hkv, N = 256, 8, 4096
     wl = Workload(f"g{G}_d{d}", B, G * Hkv, Hkv, d, N, 0, 0)
     cache = Cache(B, wl.Hq, Hkv, d, N, out_dtype="bf16", kernel=kernel)
