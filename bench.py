@@ -429,7 +429,8 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "kernel": f"lf decode ({plan['kernel']})",
-                     "alg_bytes_per_launch": alg},
+                     "alg_bytes_per_launch": alg,
+                     "frac_of_nominal_8tbs": achieved / 8000.0},   # north star quotes B200's ~8 TB/s
         "hbm_gbs_aggregate": achieved * args.gpus,
         "e2e": e2e,
         "gpu_launches": args.steps * cache.kernels_per_step(),
