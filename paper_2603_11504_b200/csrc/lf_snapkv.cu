@@ -33,8 +33,8 @@ struct SnapParams {
     uint16_t* V;
     int32_t* n_valid;       // [B][Hkv]
     int32_t* kept;          // [Hkv][N] or nullptr
-    float* part;            // [Hkv][tiles][R][2]
-    float* rows;            // [Hkv][R][2]  (M, 1/Z)
+    float* part;            // [Hkv][tiles][R][2] per-tile (max, sum 2^(t - max)) in log2 units
+    float* rows;            // [Hkv][R] log2 of the row softmax denominators (M + log2 Z, log2 units)
     float* score;           // [Hkv][np]
     float* pooled;          // [Hkv][np]
     int32_t* kidx;          // [Hkv][N] scratch
@@ -86,11 +86,8 @@ __global__ void __launch_bounds__(128) snapkv_logits_tc(SnapParams p, int pass) 
     if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(tslot), 128);
     stage_rows_sw128(kt, p.k + ((size_t)h * n + i0) * D, min(kTile, n - i0), D, tid, 128);
     stage_rows_sw128(qo, p.q_obs + (size_t)h * R * D, R, D, tid, 128);
-    if (pass == 1)
-        for (int r = tid; r < R; r += 128) {
-            rs[2 * r] = p.rows[((size_t)h * R + r) * 2];
-            rs[2 * r + 1] = p.rows[((size_t)h * R + r) * 2 + 1];
-        }
+    if (pass == 1)   // per-row offset M_r + log2 Z_r (log2 units)
+        for (int r = tid; r < R; r += 128) rs[r] = p.rows[(size_t)h * R + r];
     cp_async_commit();
     cp_async_wait<0>();
     ptx::fence_proxy_async_smem();   // generic-proxy SMEM writes -> visible to the tensor core
@@ -114,6 +111,7 @@ __global__ void __launch_bounds__(128) snapkv_logits_tc(SnapParams p, int pass) 
     ptx::tc_fence_after();
     const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);   // this warp's 32 TMEM lanes
     const int lrow = 32 * warp + lane;                           // TMEM lane of this thread
+    const float sl2 = p.scale * 1.4426950408889634f;            // logits in log2 units
     if (pass == 0) {
         // thread = observation row r; columns = the tile's tokens
         const int r = lrow;
@@ -124,18 +122,29 @@ __global__ void __launch_bounds__(128) snapkv_logits_tc(SnapParams p, int pass) 
             uint32_t v[16];
             ptx::tmem_ld_x16(tl + (uint32_t)c0, v);
             ptx::tmem_ld_wait();
+            if (c0 + 16 <= jmax) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < jmax) m = fmaxf(m, __uint_as_float(v[j]) * p.scale);
+                for (int j = 0; j < 16; ++j) m = fmaxf(m, __uint_as_float(v[j]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < jmax) m = fmaxf(m, __uint_as_float(v[j]));
+            }
         }
+        m *= sl2;   // scale > 0: the max commutes with the scaling
         float z = 0.f;
         for (int c0 = 0; c0 < kTile; c0 += 16) {
             uint32_t v[16];
             ptx::tmem_ld_x16(tl + (uint32_t)c0, v);
             ptx::tmem_ld_wait();
+            if (c0 + 16 <= jmax) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < jmax) z += expf(__uint_as_float(v[j]) * p.scale - m);
+                for (int j = 0; j < 16; ++j) z += ptx::ex2_approx(fmaf(__uint_as_float(v[j]), sl2, -m));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < jmax) z += ptx::ex2_approx(fmaf(__uint_as_float(v[j]), sl2, -m));
+            }
         }
         if (r < R) {
             float* pr = p.part + (((size_t)h * p.tiles + t) * R + r) * 2;
@@ -143,16 +152,21 @@ __global__ void __launch_bounds__(128) snapkv_logits_tc(SnapParams p, int pass) 
             pr[1] = z;
         }
     } else {
-        // thread = token i; columns = observation rows
+        // thread = token i; columns = observation rows; alpha_ri = 2^(t_ri - (M_r + log2 Z_r))
         const int i = i0 + lrow;
         float acc = 0.f;
         for (int c0 = 0; c0 < R; c0 += 16) {
             uint32_t v[16];
             ptx::tmem_ld_x16(tl + (uint32_t)c0, v);
             ptx::tmem_ld_wait();
+            if (c0 + 16 <= R) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (c0 + j < R) acc += expf(__uint_as_float(v[j]) * p.scale - rs[2 * (c0 + j)]) * rs[2 * (c0 + j) + 1];
+                for (int j = 0; j < 16; ++j) acc += ptx::ex2_approx(fmaf(__uint_as_float(v[j]), sl2, -rs[c0 + j]));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (c0 + j < R) acc += ptx::ex2_approx(fmaf(__uint_as_float(v[j]), sl2, -rs[c0 + j]));
+            }
         }
         if (i < np) p.score[(size_t)h * np + i] = acc / (float)R;
     }
@@ -183,7 +197,7 @@ __global__ void __launch_bounds__(256) snapkv_rowstats(SnapParams p) {
             const float2 pr = *(const float2*)(p.part + (((size_t)h * p.tiles + t) * R + r) * 2);
             if (pr.x == -INFINITY) continue;
             const float nm = fmaxf(M, pr.x);
-            Z = Z * expf(M - nm) + pr.y * expf(pr.x - nm);
+            Z = Z * exp2f(M - nm) + pr.y * exp2f(pr.x - nm);
             M = nm;
         }
     }
@@ -195,9 +209,8 @@ __global__ void __launch_bounds__(256) snapkv_rowstats(SnapParams p) {
         for (int q = 0; q < 8; ++q) MM = fmaxf(MM, sm[q][rl]);
         float ZZ = 0.f;
         for (int q = 0; q < 8; ++q)
-            if (sm[q][rl] != -INFINITY) ZZ += sz[q][rl] * expf(sm[q][rl] - MM);
-        p.rows[((size_t)h * R + r) * 2] = MM;
-        p.rows[((size_t)h * R + r) * 2 + 1] = 1.0f / ZZ;
+            if (sm[q][rl] != -INFINITY) ZZ += sz[q][rl] * exp2f(sm[q][rl] - MM);
+        p.rows[(size_t)h * R + r] = MM + log2f(ZZ);   // log2 of the row's softmax denominator
     }
 }
 
