@@ -955,6 +955,10 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                 // persistent loop is correct either way (no cross-cluster dependency).
                 if (k == 2) C *= 2;
                 if (C <= 0) continue;
+                if (const char* f = getenv("LF_FORCE_PLAN")) {   // debug: "S,k,solo"
+                    int fs = 0, fk = 0, fo = -1;
+                    if (sscanf(f, "%d,%d,%d", &fs, &fk, &fo) == 3 && (fs != splits || fk != k || fo != solo)) continue;
+                }
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
                 long long cost, R = 0;
                 int Cu;
