@@ -10,9 +10,12 @@ A "step" is one lf_decode_step over every (sequence, kv head) unit of the rank's
 hot path (logits, softmax, PV, LongFlowScore, argmin, in-place eviction) on a FULL static cache,
 so every step evicts.  value = tokens/s summed over ranks (one token per sequence per step).
 Inputs of 8 pre-generated steps live in HBM; the cache (8.6 GB per GPU for `r`) is far larger
-than L2, so no L2 flush is needed between steps.  Caches below FLUSH_BELOW bytes per GPU (`tiny`, `q7`,
-small sweep points) would sit in the 126 MB L2 across steps: there every timed step is preceded by an
-untimed 512 MB read (L2 flush) and bracketed by its own CUDA events; ms_per_step is their mean.
+than L2, so no L2 flush is needed between steps.  Caches below FLUSH_BELOW bytes per GPU would sit in
+the 126 MB L2 across steps.  For them the bench cycles L = ceil(4 x L2 / cache)
+layer caches of the same shape -- like the L layers of a model, each layer's cache is cold in L2 when
+its step runs -- in one CUDA graph of K x L back-to-back steps; ms_per_step = time / (K x L).  When L
+would exceed MAX_LAYERS (`tiny`), every timed step is instead preceded by an untimed 512 MB read (L2
+flush) and bracketed by its own CUDA events; ms_per_step is their mean.
 """
 from __future__ import annotations
 
@@ -213,7 +216,17 @@ def run_reference(args, wl, B_total):
     return 0
 
 
-FLUSH_BELOW = 512 << 20   # cache bytes per GPU under which steps are timed one by one after an L2 flush
+FLUSH_BELOW = 512 << 20   # cache bytes per GPU under which the cache would stay L2-resident across steps
+L2_BYTES = 126 << 20
+MAX_LAYERS = 256
+
+
+def layers_for(cb):
+    """Layer caches to cycle so that their total is >= 4 x L2 (0: use the flush method)."""
+    if cb >= FLUSH_BELOW:
+        return 1
+    L = -(-4 * L2_BYTES // max(cb, 1))
+    return L if L <= MAX_LAYERS else 0
 
 
 def cache_bytes_per_gpu(wl, B):
@@ -223,6 +236,10 @@ def cache_bytes_per_gpu(wl, B):
 def l2_note(cb):
     if cb >= FLUSH_BELOW:
         return "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(cb / 1e9)
+    L = layers_for(cb)
+    if L:
+        return ("{} layer caches of {:.1f} MB cycled back to back in one CUDA graph ({:.0f} MB > 4 x L2): "
+                "each step's cache is cold in L2, as in an L-layer model".format(L, cb / 1e6, L * cb / 1e6))
     return ("L2 flushed before every timed step (512 MB read, untimed; cache {:.1f} MB per GPU); "
             "per-step CUDA events, no graph".format(cb / 1e6))
 
@@ -256,7 +273,8 @@ def config_of(args, wl, B_total, plan):
          "num_q_heads": wl.Hq, "num_kv_heads": wl.Hkv, "head_dim": wl.d, "budget": wl.N,
          "cache": "full (every step evicts)", "out_dtype": args.out_dtype,
          "parallelism": f"dp{args.gpus} by sequence (no collective on the hot path)",
-         "l2": l2_note(cache_bytes_per_gpu(wl, B_total // max(args.gpus, 1)))}
+         "l2": l2_note(cache_bytes_per_gpu(wl, B_total // max(args.gpus, 1))),
+         "layer_caches": max(layers_for(cache_bytes_per_gpu(wl, B_total // max(args.gpus, 1))), 1)}
     if plan:
         c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"],
                   "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1})
@@ -336,25 +354,47 @@ def main():
     pool = [syn.step() for _ in range(8)]
     out, slot, _ = cache.new_outputs()
     stream = torch.cuda.Stream(device=dev)
+    # L2-resident cache: L layer caches of the same shape, cycled like the layers of a model
+    n_layers = layers_for(cache_bytes_per_gpu(wl, B))
+    layers = [cache]
+    for _ in range(1, max(n_layers, 1)):
+        c2 = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
+                   split_tokens=args.split_tokens, device=local, mode=args.mode)
+        K2, V2, nv2 = c2.views()
+        K2.copy_(K)
+        V2.copy_(V)
+        nv2.copy_(nv)
+        if args.mode != "same_step":
+            c2.pending().zero_()
+        layers.append(c2)
     torch.cuda.synchronize(dev)
 
     def step(i):
         q, kn, vn = pool[i % len(pool)]
         cache.decode_step(q, kn, vn, out, slot, stream=stream)
 
+    def layer_steps(i):   # one decode step of every layer cache (K x L launches per graph)
+        q, kn, vn = pool[i % len(pool)]
+        for c in layers:
+            c.decode_step(q, kn, vn, out, slot, stream=stream)
+
     # warm-up (W steps), then optionally capture a graph of the K timed steps (launch-bound configs)
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize(dev)
     flush = None
-    if cache_bytes_per_gpu(wl, B) < FLUSH_BELOW:
+    if n_layers == 0:
         flush = torch.zeros(128 << 20, dtype=torch.float32, device=dev)
+    elif n_layers > 1:
+        for i in range(args.warmup):
+            layer_steps(i)
+        torch.cuda.synchronize(dev)
     graph = None
     if not args.no_graph and flush is None:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=stream):
             for i in range(args.steps):
-                step(i)
+                layer_steps(i) if n_layers > 1 else step(i)
         torch.cuda.synchronize(dev)
         graph.replay()     # one untimed replay (graph upload)
         torch.cuda.synchronize(dev)
@@ -370,10 +410,11 @@ def main():
                 graph.replay()
         else:
             for j in range(args.steps):
-                step(j)
+                layer_steps(j) if n_layers > 1 else step(j)
 
+    steps_timed = args.steps * max(n_layers, 1)
     with ClockSampler(local) as clk:
-        ms = timed_steps(run_all, args.steps, stream, flush) * args.steps
+        ms = timed_steps(run_all, steps_timed, stream, flush) * steps_timed
     if pg:
         pg.barrier()
     ms_max = lfd.max_over_ranks(ms, device=dev)
@@ -389,7 +430,7 @@ def main():
         torch.cuda.synchronize(dev)
         gather = {"us": lfd.max_over_ranks(g0.elapsed_time(g1) * 1e3, device=dev),
                   "bytes": out_all.numel() * out_all.element_size() + slot_all.numel() * 4}
-    ms_step = ms_max / args.steps
+    ms_step = ms_max / steps_timed
     value = B_total / (ms_step / 1e3)
 
     # ---- end to end through the public host API: H2D of the step's inputs + D2H of out/slot
@@ -404,9 +445,9 @@ def main():
     if pg:
         pg.barrier()
     torch.cuda.synchronize(dev)
-    def e2e_run(i):
-        for _ in range(1 if i is not None else e2e_steps):
-            cache.decode_step_host(*hq, oh, sh, stream=stream)
+    def e2e_run(i):   # cycles the layer caches like the timed region (each step's cache cold in L2)
+        for j in range(1 if i is not None else e2e_steps):
+            layers[j % len(layers)].decode_step_host(*hq, oh, sh, stream=stream)
 
     e_ms = torch.tensor([lfd.max_over_ranks(timed_steps(e2e_run, e2e_steps, stream, flush), device=dev)])
     h2d = sum(t.numel() * t.element_size() for t in hq)
@@ -433,7 +474,7 @@ def main():
                      "frac_of_nominal_8tbs": achieved / 8000.0},   # north star quotes B200's ~8 TB/s
         "hbm_gbs_aggregate": achieved * args.gpus,
         "e2e": e2e,
-        "gpu_launches": args.steps * cache.kernels_per_step(),
+        "gpu_launches": steps_timed * cache.kernels_per_step(),
         "clocks": clk.summary(),
         "graph": graph is not None,
     }

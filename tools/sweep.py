@@ -9,7 +9,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
-from bench import FLUSH_BELOW, alg_bytes_per_step, cache_bytes_per_gpu, l2_note, peaks, timed_steps
+from bench import alg_bytes_per_step, cache_bytes_per_gpu, l2_note, layers_for, peaks, timed_steps
 from lf_synth import Synth, random_cache, sweep_workload
 from paper_2603_11504_b200 import Cache
 
@@ -37,26 +37,41 @@ for N in map(int, args.budgets.split(",")):
             cache.decode_step(*pool[i % 4], out, slot, stream=st)
         torch.cuda.synchronize()
         flush = g = None
-        if cache_bytes_per_gpu(wl, B) < FLUSH_BELOW:   # L2-resident cache: flush before every step
+        cb = cache_bytes_per_gpu(wl, B)
+        L = layers_for(cb)
+        layers = [cache]
+        for _ in range(1, max(L, 1)):   # L2-resident cache: cycle L layer caches (bench.py, D.4)
+            c2 = Cache(B, wl.Hq, wl.Hkv, wl.d, N, out_dtype="bf16")
+            K2, V2, nv2 = c2.views()
+            K2.copy_(K); V2.copy_(V); nv2.copy_(nv)
+            layers.append(c2)
+        steps = max(3, min(args.steps, 2000 // max(L, 1)))   # bounded graph size (<= ~2000 launches)
+        if L == 0:
             flush = torch.zeros(128 << 20, dtype=torch.float32, device="cuda")
             run = lambda i: cache.decode_step(*pool[i % 4], out, slot, stream=st)
         else:
+            for i in range(3):
+                for c in layers:
+                    c.decode_step(*pool[i % 4], out, slot, stream=st)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=st):
-                for i in range(args.steps):
-                    cache.decode_step(*pool[i % 4], out, slot, stream=st)
+                for i in range(steps):
+                    for c in layers:
+                        c.decode_step(*pool[i % 4], out, slot, stream=st)
             g.replay(); torch.cuda.synchronize()
 
             def run(i):
                 with torch.cuda.stream(st):
                     g.replay()
-        us = timed_steps(run, args.steps, st, flush) * 1e3
+        us = timed_steps(run, steps * max(L, 1), st, flush) * 1e3
         alg = alg_bytes_per_step(wl, B, 2)
         rec = {"B": B, "N": N, "latency_us": us, "tokens_per_s": B / (us * 1e-6), "alg_bytes": alg,
                "GBps": alg / (us * 1e-6) / 1e9, "frac_measured_peak": alg / (us * 1e-6) / 1e9 / peak,
-               "plan": cache.plan(), "l2": l2_note(cache_bytes_per_gpu(wl, B))}
+               "plan": cache.plan(), "l2": l2_note(cb), "layer_caches": max(L, 1)}
         print(json.dumps(rec), flush=True)
         f.write(json.dumps(rec) + "\n")
-        cache.close()
-        del cache, K, V, nv, pool, out, slot, flush, g
+        f.flush()
+        for c in layers:
+            c.close()
+        del cache, K, V, nv, pool, out, slot, flush, g, layers
         torch.cuda.empty_cache()
