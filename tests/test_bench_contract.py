@@ -43,3 +43,16 @@ def test_warmup_floor():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--warmup", "2"], capture_output=True,
                        text=True, timeout=120, cwd=ROOT)
     assert r.returncode != 0 and "warmup" in r.stderr
+
+
+def test_l2_methods():
+    """Caches larger than L2 run back to back; L2-resident ones cycle >= 4 x L2 of layer caches; only
+    caches too small for <= 256 layers fall back to per-step timing after an L2 flush."""
+    big = bench.cache_bytes_per_gpu(CONFIGS["r"], 256)
+    assert big > bench.FLUSH_BELOW and bench.layers_for(big) == 1
+    q7 = bench.cache_bytes_per_gpu(CONFIGS["q7"], 1)
+    L = bench.layers_for(q7)
+    assert 1 < L <= bench.MAX_LAYERS and L * q7 >= 4 * bench.L2_BYTES
+    assert bench.layers_for(bench.cache_bytes_per_gpu(CONFIGS["tiny"], 1)) == 0
+    assert "flushed" in bench.l2_note(bench.cache_bytes_per_gpu(CONFIGS["tiny"], 1))
+    assert "layer caches" in bench.l2_note(q7) and "larger than L2" in bench.l2_note(big)
