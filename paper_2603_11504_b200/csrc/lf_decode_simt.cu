@@ -20,6 +20,8 @@
 //           lowest index on exact ties (R7).
 //   write   rank 0: out = (sum_s o_s 2^(m_s - M) + 2^(x* - M) v*) / Z, slot, in-place eviction
 //           write of (k*, v*) into the victim (Fig. 2) or append at n (R11).
+#include <mutex>
+
 #include "lf_common.cuh"
 
 namespace lf {
@@ -274,21 +276,22 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
 template <int D, int GP>
 cudaError_t launch_t(const StepParams& p, const Plan& plan, cudaStream_t stream) {
     auto kern = simt_decode_kernel<D, GP>;
-    // kernel attributes are per device; set them once (host-side, outside any stream capture)
-    static int smem_set[64] = {0};
-    static bool np_set[64] = {false};
+    // kernel attributes are per device: set once to the largest values any plan uses, under a lock
+    // (host-side, outside any stream capture; concurrent cache creation is race-free)
+    static std::mutex mu;
+    static bool done[64] = {false};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (dev < 64 && plan.smem > smem_set[dev]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem);
-        if (e != cudaSuccess) return e;
-        smem_set[dev] = plan.smem;
-    }
-    if (plan.splits > 8 && dev < 64 && !np_set[dev]) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        np_set[dev] = true;
+    if (dev >= 64) return cudaErrorInvalidDevice;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!done[dev]) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            if (e != cudaSuccess) return e;
+            done[dev] = true;
+        }
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.splits * p.B * p.Hkv, 1, 1);   // cluster (splits,1,1) = one unit

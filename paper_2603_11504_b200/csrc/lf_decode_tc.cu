@@ -30,6 +30,8 @@
 #include <stdlib.h>
 #include <cudaTypedefs.h>
 
+#include <mutex>
+
 #include "lf_common.cuh"
 #include "lf_tc_ptx.cuh"
 
@@ -788,26 +790,27 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
 
 __host__ __device__ constexpr int gpad_tc(int G) { return G <= 4 ? 4 : 8; }
 
+// Kernel attributes are per device: set once, to the largest values any plan uses (the dynamic SMEM
+// of a launch is still the plan's own), under a lock so concurrent cache creation is race-free.
 template <int GP, int NG>
 cudaError_t set_attrs(int smem, int splits) {
-    static int smem_set[64] = {0};
-    static bool np_set[64] = {false};
+    (void)smem;
+    (void)splits;
+    static std::mutex mu;
+    static bool done[64] = {false};
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    if (dev >= 64 || smem > smem_set[dev]) {
-        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
+    if (dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done[dev]) return cudaSuccess;
+    e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e != cudaSuccess) return e;
-        if (dev < 64) smem_set[dev] = smem;
-    }
-    if (splits > 8 && (dev >= 64 || !np_set[dev])) {
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        if (dev < 64) np_set[dev] = true;
-    }
-    return cudaSuccess;
+    if (e == cudaSuccess) done[dev] = true;
+    return e;
 }
 
 template <int GP, int NG>
@@ -859,14 +862,14 @@ cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) 
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {   // thread-safe one-time lookup
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
             q == cudaDriverEntryPointSuccess)
-            fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
-    }
+            return (PFN_cuTensorMapEncodeTiled_v12000)f;
+        return (PFN_cuTensorMapEncodeTiled_v12000) nullptr;
+    }();
     return fn;
 }
 
