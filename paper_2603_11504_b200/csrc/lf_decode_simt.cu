@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
     const int s = (int)cluster.block_rank();
     const int u = blockIdx.x / S;
     const int b = u / p.Hkv, h = u % p.Hkv;
-    pdl_trigger();
-    pdl_wait();   // the previous step's cache writes are visible from here on
+    pdl_trigger();   // the next step's prologue may overlap this step (this kernel never speculates)
+    pdl_wait();      // the previous step's cache writes are visible from here on
     const int n = p.n_valid[u];
     const int c0 = s * chunk;
     const int c1 = min(c0 + chunk, N);
@@ -315,6 +315,7 @@ Plan simt_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     pl.stages = 2;
     pl.tmem_cols = 0;
     pl.solo_rounds = 0;
+    pl.lat = 0;
     const int GP = gpad(G);
     const int fixed = simt_smem(d, GP, G, 0).total;
     int chunk_max = (kMaxSmem - fixed) / ((G + 1) * 4) / 128 * 128;

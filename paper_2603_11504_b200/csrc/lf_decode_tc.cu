@@ -90,16 +90,19 @@ constexpr int EMPTY = FULL + kMaxStages;
 constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kMaxNG;
 constexpr int QFULL = PFREE + kMaxNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
 constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
-constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
+constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2;
+constexpr int SPEC = XFREE + 2;         // [kMaxStages] first ring pass: speculative TMA landed / released
+constexpr int NBARS = SPEC + kMaxStages;
 static_assert(NBARS <= 48, "barrier slots");
 
-// Debug event trace (-DLF_TRACE): %globaltimer at fixed points, [cta][unit % 64][32] u64.
+// Debug event trace (-DLF_TRACE): %clock64 at fixed points, [cta][unit % 64][32] u64; slot 31 of
+// row 0 holds the %globaltimer at slot 16 (entry) so tools/trace_run.py can align the CTAs.
 #ifdef LF_TRACE
 #define LF_EVENT(ui_, slot_)                                                                   \
     do {                                                                                       \
         if (p.trace) {                                                                         \
             unsigned long long t_;                                                             \
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                \
             p.trace[((size_t)blockIdx.x * 64 + ((ui_) & 63)) * 32 + (slot_)] = t_;             \
         }                                                                                      \
     } while (0)
@@ -166,7 +169,11 @@ __host__ __device__ inline int tc_hold(int N, int chunk, int solo_rounds) {
     return solo_rounds > 0 && Nr > chunk ? Nr : chunk;
 }
 
-template <int GP, int kNG>
+// kLat: the latency variant for grids that leave SMs free (small batches): speculative first tiles,
+// per-role PDL waits after a parameter-only setup, one-round-trip operand loads, 16-lane x* / (M, Z)
+// reductions and a thread-per-element split combine.  Machine-filling grids use kLat = false, which
+// is the streaming-tuned code (measured: the latency changes cost 1-3 % there).
+template <int GP, int kNG, bool kLat>
 __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     constexpr int kNS = 128 * kNG;          // softmax threads
     extern __shared__ unsigned char smem_raw[];
@@ -217,12 +224,44 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         }
         ptx::mbar_init(BAR(OFULL), 1);
         ptx::mbar_init(BAR(OFREE), 4);
+        if constexpr (kLat)
+            for (int i = 0; i < ST; ++i) ptx::mbar_init(BAR(SPEC + i), 1);
         ptx::fence_mbar_init();
         ptx::tma_prefetch_desc(&a.tmK);
         ptx::tma_prefetch_desc(&a.tmV);
     }
+    // Speculative first tiles (same-step mode): issue the first item's first ring stages BEFORE the
+    // PDL wait, so their HBM latency overlaps the previous step's tail.  Only a unit that was full
+    // before the previous step is speculated: n never decreases between decode steps and stays N once
+    // full, so its tile count is final.  The only row of it the previous step (the one kernel that may
+    // still run: every decode kernel triggers its dependents after its own wait) can have written is
+    // wrote[u]; the producer re-reads that row after the wait and patches it into the stage before
+    // releasing the stage (FULL).  TMA completion of a speculative stage lands on SPEC.  Only grids
+    // that leave SMs free speculate (the next step's CTAs can then start during this one).
+    int nspec = 0;
+    if (kLat && tid == 0 && p.spec) {
+        const UnitInfo x = item_base(p, cid, s, C, 0);
+        if (x.valid && __ldcg(p.n_valid + x.u) >= N) {
+            const int nt = (x.c1 - x.c0 + 127) / 128;
+            nspec = min(2 * nt, ST);
+            for (int j = 0; j < nspec; ++j) {
+                const int tile = j < nt ? j : j - nt;
+                ptx::mbar_arrive_expect_tx(BAR(SPEC + j), kStageBytes);
+                ptx::tma_load_3d(ring + (uint32_t)j * kStageBytes, j < nt ? (const void*)&a.tmK : (const void*)&a.tmV,
+                                 BAR(SPEC + j), 0, x.u * N + x.c0 + tile * 128, 0);
+            }
+        }
+    }
+    if (kLat && tid == 0) *(volatile int*)(smem + so.tmem + 4) = nspec;   // read by every role after the cluster sync
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(smem + so.tmem), (uint32_t)a.tmem_cols);
     if (tid == 0) LF_EVENT(0, 16);
+#ifdef LF_TRACE
+    if (tid == 0 && p.trace) {   // SM cycles above; one globaltimer stamp per CTA aligns the CTAs
+        unsigned long long g_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));
+        p.trace[((size_t)blockIdx.x * 64) * 32 + 31] = g_;
+    }
+#endif
     if (tid == 64) {   // L2 warm-up of the first item's operands; safe before the PDL wait (L2 is coherent)
         const UnitInfo x = item_base(p, cid, s, C, 0);
         if (x.valid) {
@@ -248,54 +287,158 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     ptx::cluster_sync_all();   // barriers of every rank initialised before any remote arrival
     ptx::tc_fence_after();
     if (tid == 0) LF_EVENT(0, 17);
-    pdl_trigger();             // the next step's prologue may overlap this step
-    pdl_wait();                // the previous step's cache writes are visible from here on
-    if (tid == 0) LF_EVENT(0, 18);
+    // Each role runs its parameter-only setup (first item's indices and pointers) BEFORE its PDL
+    // wait, then waits: from there on the previous step's cache writes are visible.  A speculating
+    // step triggers its dependents only after its wait, so when a step starts speculating, the
+    // only step of the same cache that can still be running is the one just before it (steps of
+    // one cache share a plan, so they all speculate or none does; a chain of early-triggering
+    // steps of other caches ends at the first speculating one).
+    if constexpr (!kLat) {
+        pdl_trigger();             // the next step's prologue may overlap this step
+        pdl_wait();                // the previous step's cache writes are visible from here on
+    }
     const uint32_t tmem = *(volatile uint32_t*)(smem + so.tmem);
+    if constexpr (kLat) nspec = *(volatile int*)(smem + so.tmem + 4);   // speculative ring indices [0, nspec)
+    const UnitInfo x0 = item_base(p, cid, s, C, 0);
+    auto dep_wait = [&]() {
+        if constexpr (kLat) {
+            // the empty asm statements consume the setup values, so they are computed (and the kernel
+            // parameters they read are in the constant cache) before the wait -- nvcc otherwise sinks them
+            asm volatile("" ::"r"(x0.u), "r"(x0.b), "r"(x0.h), "r"(x0.c0), "r"(x0.c1), "r"((int)x0.valid));
+            asm volatile("" ::"l"(p.q), "l"(p.k_new), "l"(p.v_new), "l"(p.n_valid), "l"(p.out), "l"(p.wrote));
+            asm volatile("" ::"r"(p.Hq), "r"(p.N), "r"(p.chunk), "r"(p.out_f32), "f"(p.scale_log2), "l"(p.scores));
+            if (p.spec) {   // speculating steps trigger after the wait (at most one earlier step runs)
+                pdl_wait();
+                pdl_trigger();
+            } else {
+                pdl_trigger();
+                pdl_wait();
+            }
+        }
+    };
 
     if (warp == 0) {
         // ------------------------------ producer -------------------------------------------------
-        uint32_t it = 0, qi = 0;
-        for (int i = 0;; ++i, ++qi) {
-            const UnitInfo x = item_info(p, cid, s, C, i);
-            if (!x.valid) break;
-            const int u = x.u;
-            const int qb = qi & 1;
-            // the first ring stages go out before Q is staged (they do not depend on it)
-            const int pre = min(2 * x.ntiles, ST);
-            auto issue = [&](int i) {
-                const int st = it % ST;
-                ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
-                ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
-                const int tile = i < x.ntiles ? i : i - x.ntiles;
-                const int row = u * N + x.c0 + tile * 128;
-                const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
-                const uint32_t dst = ring + (uint32_t)st * kStageBytes;
-                LF_TILE_EVENT(qi, 34, i);
-                ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
-                ++it;
-            };
-            if (lane == 0)
-                for (int i = 0; i < pre; ++i) issue(i);
-            ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
-            // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
-            const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
-            unsigned char* qd = smem + so.q + qb * 4096;
-            for (int e = lane; e < G * 16; e += 32) {
-                const int g = e >> 4, c = e & 15;
-                *(uint4*)(qd + (c >> 3) * 1024 + g * 128 + (((c & 7) ^ g) << 4)) = __ldg(qg + e);
+        if constexpr (kLat) {
+            uint32_t it = 0, qi = 0;
+            dep_wait();
+            if (lane == 0) LF_EVENT(0, 18);
+            for (int i = 0;; ++i, ++qi) {
+                // every global read of the item goes out at once (Q rows, fill state, last written slot):
+                // one L2 round trip instead of a chain of them before the first MMA
+                UnitInfo x = item_base(p, cid, s, C, i);
+                if (!x.valid) break;
+                const int u = x.u;
+                const int qb = qi & 1;
+                const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
+                uint4 qv[4];
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) qv[k] = lane + 32 * k < G * 16 ? __ldg(qg + lane + 32 * k) : make_uint4(0, 0, 0, 0);
+                const bool spec_item = i == 0 && nspec > 0;
+                const int ws = spec_item ? __ldcg(p.wrote + u) : -1;
+                x.n = __ldcg(p.n_valid + u);
+                x.nv = max(0, min(x.c1, x.n) - x.c0);
+                x.ntiles = (x.nv + 127) / 128;
+                if (lane == 0 && i == 0) LF_EVENT(0, 22);
+                // the first ring stages go out before Q is staged (they do not depend on it)
+                const int pre = min(2 * x.ntiles, ST);
+                auto issue = [&](int i) {
+                    const int st = it % ST;
+                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                    ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
+                    const int tile = i < x.ntiles ? i : i - x.ntiles;
+                    const int row = u * N + x.c0 + tile * 128;
+                    const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
+                    const uint32_t dst = ring + (uint32_t)st * kStageBytes;
+                    LF_TILE_EVENT(qi, 34, i);
+                    ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
+                    ++it;
+                };
+                int first = 0;
+                if (spec_item) {
+                    // speculative stages: patch the row the previous step wrote (if it lies in one), release
+                    for (int j = 0; j < nspec; ++j) {
+                        const int tile = j < x.ntiles ? j : j - x.ntiles;
+                        const int r = ws - x.c0 - tile * 128;
+                        if (r >= 0 && r < 128 && p.spec == 1) {   // warp-uniform (spec 2: debug, no patch)
+                            const uint16_t* src = (j < x.ntiles ? p.K : p.V) + ((size_t)u * N + ws) * 128;
+                            const uint4 w = lane < 16 ? __ldcg((const uint4*)src + lane) : make_uint4(0, 0, 0, 0);
+                            ptx::mbar_wait(BAR(SPEC + j), 0);   // landed: the TMA must not overwrite the patch
+                            if (lane < 16)
+                                *(uint4*)(smem + so.ring + j * kStageBytes + (lane >> 3) * kBoxBytes + r * 128 +
+                                          (((lane & 7) ^ (r & 7)) << 4)) = w;
+                            ptx::fence_proxy_async_smem();
+                            __syncwarp();
+                        }
+                        if (lane == 0) ptx::mbar_arrive(BAR(FULL + j));
+                    }
+                    it = (uint32_t)nspec;
+                    first = nspec;
+                }
+                if (lane == 0)
+                    for (int i = first; i < pre; ++i) issue(i);
+                ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
+                if (lane == 0 && i == 0) LF_EVENT(0, 24);
+                // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
+                unsigned char* qd = smem + so.q + qb * 4096;
+    #pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = lane + 32 * k, g = e >> 4, c = e & 15;
+                    if (e < G * 16) *(uint4*)(qd + (c >> 3) * 1024 + g * 128 + (((c & 7) ^ g) << 4)) = qv[k];
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    LF_EVENT(qi, 6);
+                    ptx::mbar_arrive(BAR(QFULL + qb));
+                    for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
+                }
+                it = __shfl_sync(0xffffffffu, it, 0);
             }
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                LF_EVENT(qi, 6);
-                ptx::mbar_arrive(BAR(QFULL + qb));
-                for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
+        } else {
+            uint32_t it = 0, qi = 0;
+            for (int i = 0;; ++i, ++qi) {
+                const UnitInfo x = item_info(p, cid, s, C, i);
+                if (!x.valid) break;
+                const int u = x.u;
+                const int qb = qi & 1;
+                // the first ring stages go out before Q is staged (they do not depend on it)
+                const int pre = min(2 * x.ntiles, ST);
+                auto issue = [&](int i) {
+                    const int st = it % ST;
+                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                    ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
+                    const int tile = i < x.ntiles ? i : i - x.ntiles;
+                    const int row = u * N + x.c0 + tile * 128;
+                    const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
+                    const uint32_t dst = ring + (uint32_t)st * kStageBytes;
+                    LF_TILE_EVENT(qi, 34, i);
+                    ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
+                    ++it;
+                };
+                if (lane == 0)
+                    for (int i = 0; i < pre; ++i) issue(i);
+                ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
+                // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
+                const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
+                unsigned char* qd = smem + so.q + qb * 4096;
+                for (int e = lane; e < G * 16; e += 32) {
+                    const int g = e >> 4, c = e & 15;
+                    *(uint4*)(qd + (c >> 3) * 1024 + g * 128 + (((c & 7) ^ g) << 4)) = __ldg(qg + e);
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    LF_EVENT(qi, 6);
+                    ptx::mbar_arrive(BAR(QFULL + qb));
+                    for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
+                }
+                it = __shfl_sync(0xffffffffu, it, 0);
             }
-            it = __shfl_sync(0xffffffffu, it, 0);
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------------------------
+        dep_wait();
         if (lane == 0) {
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
@@ -314,6 +457,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it) {                  // S^T = K_tile . Q^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                    if (it < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                     LF_TILE_EVENT(ui, 32, t);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
@@ -331,6 +475,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                    if (it < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                     const int pb = pi % kNG;
                     ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
                     ptx::tc_fence_after();
@@ -360,6 +505,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         float* gM = misc + 16;     // [16]
         float* glz = misc + 32;    // [16]
         float* gZ = misc + 48;     // [16]
+        float* gFn = misc + 96;    // [16] 2^(x_g* - M_g) (split units)
+        float* gIZ = misc + 112;   // [16] 1 / Z_g (split units)
         int* s_slot = (int*)(misc + 64);
         unsigned long long* kred = (unsigned long long*)(red + 2 * kNG * 4 * 16);
         const int box = row >> 6, cc = row & 63;
@@ -401,32 +548,72 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             return best;
         };
         uint32_t it = 0, pi = 0, ui = 0, xi = 0;
+        dep_wait();
+        if (sidx == 0) LF_EVENT(0, 19);
         for (int i = 0;; ++i, ++ui) {
-            const UnitInfo x = item_info(p, cid, s, C, i);
-            if (!x.valid) break;
+            UnitInfo x;
+            uint4* kvn = (uint4*)(smem + so.kvn);
+            if constexpr (kLat) {
+                // all global reads of the item at once: fill state, k*/v* rows, the x* operands
+                x = item_base(p, cid, s, C, i);
+                if (sidx == 0 && i == 0) LF_EVENT(0, 20);
+                if (!x.valid) break;
+                const int u = x.u;
+                uint4 kvw = make_uint4(0, 0, 0, 0);
+                if (warp == 2 + 4 * kNG - 1)   // the current token's k*, v* rows (combine + eviction write)
+                    kvw = __ldg(lane < 16 ? (const uint4*)(p.k_new + (size_t)u * 128) + lane
+                                          : (const uint4*)(p.v_new + (size_t)u * 128) + (lane - 16));
+                // current token's logit x_g* (P:50-51): 16 lanes per head, 8 elements per lane
+                const int xg = sidx >> 4, xch = sidx & 15;
+                uint4 xq = make_uint4(0, 0, 0, 0), xk = make_uint4(0, 0, 0, 0);
+                if (sidx < 128 && xg < G) {
+                    xq = __ldg((const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + xg) * 128) + xch);
+                    xk = __ldg((const uint4*)(p.k_new + (size_t)u * 128) + xch);
+                }
+                x.n = __ldcg(p.n_valid + u);
+                x.nv = max(0, min(x.c1, x.n) - x.c0);
+                x.ntiles = (x.nv + 127) / 128;
+                if (sidx == 0 && i == 0) LF_EVENT(0, 21);
+                if (warp == 2 + 4 * kNG - 1) kvn[lane] = kvw;
+                if (sidx < 128) {
+                    float acc = 0.f;
+                    const uint32_t qw[4] = {xq.x, xq.y, xq.z, xq.w}, kw[4] = {xk.x, xk.y, xk.z, xk.w};
+    #pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        acc = fmaf(__uint_as_float(qw[k] << 16), __uint_as_float(kw[k] << 16), acc);
+                        acc = fmaf(__uint_as_float(qw[k] & 0xffff0000u), __uint_as_float(kw[k] & 0xffff0000u), acc);
+                    }
+    #pragma unroll
+                    for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    if (xch == 0 && xg < G) xs[xg] = p.deferred ? -INFINITY : acc * sl2;
+                }
+            } else {
+                x = item_info(p, cid, s, C, i);
+                if (!x.valid) break;
+                const int u = x.u;
+                // stage the current token's k*, v* rows (combine + eviction write read them later)
+                if (warp == 2 + 4 * kNG - 1) {
+                    const uint4* src = lane < 16 ? (const uint4*)(p.k_new + (size_t)u * 128) + lane
+                                                 : (const uint4*)(p.v_new + (size_t)u * 128) + (lane - 16);
+                    kvn[lane] = __ldg(src);
+                }
+                // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
+                for (int g = warp - 2; g < G; g += 4 * kNG) {
+                    const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
+                    const uint16_t* kn = p.k_new + (size_t)u * 128;
+                    float acc = 0.f;
+    #pragma unroll
+                    for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+                    if (lane == 0) xs[g] = p.deferred ? -INFINITY : acc * sl2;
+                }
+            }
             const int u = x.u;
             const int nv = x.nv;
             const uint32_t par = ui & 1u;
             const uint32_t sreg = tl + par * RC;
             if (sidx == 0) LF_EVENT(ui, 0);
-            // stage the current token's k*, v* rows (combine + eviction write read them later)
-            uint4* kvn = (uint4*)(smem + so.kvn);
-            if (warp == 2 + 4 * kNG - 1) {
-                const uint4* src = lane < 16 ? (const uint4*)(p.k_new + (size_t)u * 128) + lane
-                                             : (const uint4*)(p.v_new + (size_t)u * 128) + (lane - 16);
-                kvn[lane] = __ldg(src);
-            }
-            // current token's logit x_g* (P:50-51): warp w-2 takes head g = w-2
-            for (int g = warp - 2; g < G; g += 4 * kNG) {
-                const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
-                const uint16_t* kn = p.k_new + (size_t)u * 128;
-                float acc = 0.f;
-#pragma unroll
-                for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-                if (lane == 0) xs[g] = p.deferred ? -INFINITY : acc * sl2;
-            }
             if (sidx == 0) LF_EVENT(ui, 15);
             // ---- max over the unit's logits (TMEM-resident S)
             ptx::mbar_wait(BAR(KDONE + par), (ui >> 1) & 1u);
@@ -491,6 +678,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const uint32_t iv = it + x.ntiles + t;
                 const int st = iv % ST;
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
+                if (iv < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                 if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 5);
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
@@ -590,6 +778,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int sl = x.n < N ? x.n : (int)(kb & 0xffffffffull);
                         *s_slot = sl;
                         p.slot[u] = sl;
+                        if constexpr (kLat) p.wrote[u] = sl;
                         if (x.n < N) p.n_valid[u] = x.n + 1;
                     }
                 }
@@ -663,25 +852,56 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
             float* fr = misc + 128;    // [g][r] = 2^(m_g,r - M_g)
-            for (int g = warp - 2; g < G; g += 4 * kNG) {   // one warp per head, lane r <-> rank r
-                float mr = -INFINITY, zr = 0.f;
-                if (lane < S) {
-                    mr = xc->mz[lane][g][0];
-                    zr = xc->mz[lane][g][1];
+            if constexpr (kLat) {
+                if (sidx < 128) {          // 16 lanes per head, lane r <-> rank r
+                    const int g = sidx >> 4, r = sidx & 15;
+                    float mr = -INFINITY, zr = 0.f;
+                    if (g < G && r < S) {
+                        mr = xc->mz[r][g][0];
+                        zr = xc->mz[r][g][1];
+                    }
+                    const float xsg = g < G ? xs[g] : -INFINITY;
+                    float M = fmaxf(xsg, mr);
+    #pragma unroll
+                    for (int off = 8; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                    const float f = r < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
+                    float Z = zr * f;
+    #pragma unroll
+                    for (int off = 8; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
+                    const float fn = ptx::ex2_approx(xsg - M);
+                    Z += fn;
+                    if (g < G) {
+                        if (r < S) fr[g * 16 + r] = f;
+                        if (r == 0) {
+                            gM[g] = M;
+                            gZ[g] = Z;
+                            glz[g] = log2f(Z);
+                            gFn[g] = fn;
+                            gIZ[g] = 1.0f / Z;
+                        }
+                    }
                 }
-                float M = fmaxf(xs[g], mr);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-                const float f = lane < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
-                float Z = zr * f;
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
-                Z += ptx::ex2_approx(xs[g] - M);
-                if (lane < S) fr[g * 16 + lane] = f;
-                if (lane == 0) {
-                    gM[g] = M;
-                    gZ[g] = Z;
-                    glz[g] = log2f(Z);
+            } else {
+                for (int g = warp - 2; g < G; g += 4 * kNG) {   // one warp per head, lane r <-> rank r
+                    float mr = -INFINITY, zr = 0.f;
+                    if (lane < S) {
+                        mr = xc->mz[lane][g][0];
+                        zr = xc->mz[lane][g][1];
+                    }
+                    float M = fmaxf(xs[g], mr);
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+                    const float f = lane < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
+                    float Z = zr * f;
+    #pragma unroll
+                    for (int off = 16; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
+                    Z += ptx::ex2_approx(xs[g] - M);
+                    if (lane < S) fr[g * 16 + lane] = f;
+                    if (lane == 0) {
+                        gM[g] = M;
+                        gZ[g] = Z;
+                        glz[g] = log2f(Z);
+                    }
                 }
             }
             ptx::named_bar_sync(1, kNS);
@@ -704,46 +924,84 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::st_async_u64(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, key) + 8 * s, 0), kb,
                                   ptx::mapa(BAR(KREADY + xp), 0));
             }
-            // ---- output combine of my slice from the inbox: S consecutive lanes (SG = pow2 >= S)
-            //      share one float4 element, lane r reads sender r's part
-            {
-                const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
-                const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
-                const int SG = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16;
-                const int r = lane % SG, per_warp = 32 / SG;
-                for (int e0 = ((sidx >> 5) * per_warp); e0 < cnt; e0 += (kNS >> 5) * per_warp) {
-                    const int e = e0 + lane / SG;
-                    const bool ok = e < cnt;
-                    const int i4 = i4_0 + (ok ? e : 0);
-                    const int g = i4 >> 5, l = (i4 & 31) * 4;
-                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (ok && r < S) {
-                        const float f = fr[g * 16 + r];
-                        const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
-                        acc = make_float4(o4.x * f, o4.y * f, o4.z * f, o4.w * f);
+            if constexpr (kLat) {
+                // ---- output combine of my slice from the inbox: one thread per float4 element, the S
+                //      ranks' parts accumulated in rank order
+                {
+                    const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
+                    const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
+                    for (int e = sidx; e < cnt; e += kNS) {
+                        const int i4 = i4_0 + e;
+                        const int g = i4 >> 5, l = (i4 & 31) * 4;
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    #pragma unroll 4
+                        for (int r = 0; r < S; ++r) {
+                            const float f = fr[g * 16 + r];
+                            const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
+                            acc.x = fmaf(o4.x, f, acc.x);
+                            acc.y = fmaf(o4.y, f, acc.y);
+                            acc.z = fmaf(o4.z, f, acc.z);
+                            acc.w = fmaf(o4.w, f, acc.w);
+                        }
+                        const float fn = gFn[g], invZ = gIZ[g];
+                        const uint2 vw = *(const uint2*)(vn + l);
+                        const float o0 = fmaf(fn, __uint_as_float(vw.x << 16), acc.x) * invZ;
+                        const float o1 = fmaf(fn, __uint_as_float(vw.x & 0xffff0000u), acc.y) * invZ;
+                        const float o2 = fmaf(fn, __uint_as_float(vw.y << 16), acc.z) * invZ;
+                        const float o3 = fmaf(fn, __uint_as_float(vw.y & 0xffff0000u), acc.w) * invZ;
+                        const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
+                        if (p.out_f32) {
+                            *(float4*)((float*)p.out + oi) = make_float4(o0, o1, o2, o3);
+                        } else {
+                            uint2 w;
+                            w.x = (uint32_t)f32_to_bf16_rne(o0) | ((uint32_t)f32_to_bf16_rne(o1) << 16);
+                            w.y = (uint32_t)f32_to_bf16_rne(o2) | ((uint32_t)f32_to_bf16_rne(o3) << 16);
+                            *(uint2*)((uint16_t*)p.out + oi) = w;
+                        }
                     }
-                    for (int off = SG >> 1; off > 0; off >>= 1) {
-                        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-                        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-                        acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
-                        acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
-                    }
-                    if (!ok || r != 0) continue;
-                    const float fn = ptx::ex2_approx(xs[g] - gM[g]);
-                    const uint2 vw = *(const uint2*)(vn + l);
-                    const float invZ = 1.0f / gZ[g];
-                    const float o0 = fmaf(fn, __uint_as_float(vw.x << 16), acc.x) * invZ;
-                    const float o1 = fmaf(fn, __uint_as_float(vw.x & 0xffff0000u), acc.y) * invZ;
-                    const float o2 = fmaf(fn, __uint_as_float(vw.y << 16), acc.z) * invZ;
-                    const float o3 = fmaf(fn, __uint_as_float(vw.y & 0xffff0000u), acc.w) * invZ;
-                    const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
-                    if (p.out_f32) {
-                        *(float4*)((float*)p.out + oi) = make_float4(o0, o1, o2, o3);
-                    } else {
-                        uint2 w;
-                        w.x = (uint32_t)f32_to_bf16_rne(o0) | ((uint32_t)f32_to_bf16_rne(o1) << 16);
-                        w.y = (uint32_t)f32_to_bf16_rne(o2) | ((uint32_t)f32_to_bf16_rne(o3) << 16);
-                        *(uint2*)((uint16_t*)p.out + oi) = w;
+                }
+            } else {
+                // ---- output combine of my slice from the inbox: S consecutive lanes (SG = pow2 >= S)
+                //      share one float4 element, lane r reads sender r's part
+                {
+                    const int i4_0 = s * E4, cnt = min(G * 32, i4_0 + E4) - i4_0;
+                    const uint16_t* vn = (const uint16_t*)(smem + so.kvn) + 128;
+                    const int SG = S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16;
+                    const int r = lane % SG, per_warp = 32 / SG;
+                    for (int e0 = ((sidx >> 5) * per_warp); e0 < cnt; e0 += (kNS >> 5) * per_warp) {
+                        const int e = e0 + lane / SG;
+                        const bool ok = e < cnt;
+                        const int i4 = i4_0 + (ok ? e : 0);
+                        const int g = i4 >> 5, l = (i4 & 31) * 4;
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if (ok && r < S) {
+                            const float f = fr[g * 16 + r];
+                            const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
+                            acc = make_float4(o4.x * f, o4.y * f, o4.z * f, o4.w * f);
+                        }
+                        for (int off = SG >> 1; off > 0; off >>= 1) {
+                            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+                            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+                            acc.z += __shfl_xor_sync(0xffffffffu, acc.z, off);
+                            acc.w += __shfl_xor_sync(0xffffffffu, acc.w, off);
+                        }
+                        if (!ok || r != 0) continue;
+                        const float fn = ptx::ex2_approx(xs[g] - gM[g]);
+                        const uint2 vw = *(const uint2*)(vn + l);
+                        const float invZ = 1.0f / gZ[g];
+                        const float o0 = fmaf(fn, __uint_as_float(vw.x << 16), acc.x) * invZ;
+                        const float o1 = fmaf(fn, __uint_as_float(vw.x & 0xffff0000u), acc.y) * invZ;
+                        const float o2 = fmaf(fn, __uint_as_float(vw.y << 16), acc.z) * invZ;
+                        const float o3 = fmaf(fn, __uint_as_float(vw.y & 0xffff0000u), acc.w) * invZ;
+                        const size_t oi = ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128 + l;
+                        if (p.out_f32) {
+                            *(float4*)((float*)p.out + oi) = make_float4(o0, o1, o2, o3);
+                        } else {
+                            uint2 w;
+                            w.x = (uint32_t)f32_to_bf16_rne(o0) | ((uint32_t)f32_to_bf16_rne(o1) << 16);
+                            w.y = (uint32_t)f32_to_bf16_rne(o2) | ((uint32_t)f32_to_bf16_rne(o3) << 16);
+                            *(uint2*)((uint16_t*)p.out + oi) = w;
+                        }
                     }
                 }
             }
@@ -761,6 +1019,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int sl = x.n < N ? x.n : (int)(mk & 0xffffffffull);
                         *s_slot = sl;
                         p.slot[u] = sl;
+                        if constexpr (kLat) p.wrote[u] = sl;
                         if (x.n < N) p.n_valid[u] = x.n + 1;
                     }
                 }
@@ -792,7 +1051,7 @@ __host__ __device__ constexpr int gpad_tc(int G) { return G <= 4 ? 4 : 8; }
 
 // Kernel attributes are per device: set once, to the largest values any plan uses (the dynamic SMEM
 // of a launch is still the plan's own), under a lock so concurrent cache creation is race-free.
-template <int GP, int NG>
+template <int GP, int NG, bool kLat>
 cudaError_t set_attrs(int smem, int splits) {
     (void)smem;
     (void)splits;
@@ -804,18 +1063,18 @@ cudaError_t set_attrs(int smem, int splits) {
     if (dev >= 64) return cudaErrorInvalidDevice;
     std::lock_guard<std::mutex> lock(mu);
     if (done[dev]) return cudaSuccess;
-    e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG, kLat>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG, kLat>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        e = cudaFuncSetAttribute(tc_decode_kernel<GP, NG, kLat>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e == cudaSuccess) done[dev] = true;
     return e;
 }
 
-template <int GP, int NG>
+template <int GP, int NG, bool kLat = false>
 int max_active_clusters(int splits, int smem) {
-    if (set_attrs<GP, NG>(smem, splits) != cudaSuccess) {
+    if (set_attrs<GP, NG, kLat>(smem, splits) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -831,24 +1090,24 @@ int max_active_clusters(int splits, int smem) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP, NG>, &cfg) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveClusters(&n, tc_decode_kernel<GP, NG, kLat>, &cfg) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     if (getenv("LF_DEBUG_PLAN")) {
         int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tc_decode_kernel<GP, NG>, 64 + 128 * NG, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tc_decode_kernel<GP, NG, kLat>, 64 + 128 * NG, smem);
         cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, tc_decode_kernel<GP, NG>);
+        cudaFuncGetAttributes(&fa, tc_decode_kernel<GP, NG, kLat>);
         fprintf(stderr, "[lf plan] NG=%d smem=%d blocks/SM=%d regs=%d maxdyn=%d clusters=%d\n", NG, smem, b,
                 fa.numRegs, fa.maxDynamicSharedSizeBytes, n);
     }
     return n;
 }
 
-template <int GP, int NG>
+template <int GP, int NG, bool kLat>
 cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) {
-    cudaError_t e = set_attrs<GP, NG>(plan.smem, plan.splits);
+    cudaError_t e = set_attrs<GP, NG, kLat>(plan.smem, plan.splits);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.splits * args.clusters, 1, 1);
@@ -858,7 +1117,7 @@ cudaError_t launch_t(const TcArgs& args, const Plan& plan, cudaStream_t stream) 
     cudaLaunchAttribute attr[2];
     cfg.numAttrs = fill_launch_attrs(attr, plan.splits);
     cfg.attrs = attr;
-    return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP, NG>, args);
+    return cudaLaunchKernelEx(&cfg, tc_decode_kernel<GP, NG, kLat>, args);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -912,8 +1171,8 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 1 && G <= 8; }
 // remaining units are split S ways, which balances the tail.
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     (void)d;
-    (void)num_sms;
     Plan best;
+    best.lat = 0;
     best.kernel = LF_KERNEL_TCGEN05;
     best.splits = -1;
     best.chunk = 0;
@@ -992,6 +1251,9 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         }
         if (split_tokens > 0) break;
     }
+    // latency variant when the grid leaves SMs free (the next step's CTAs can start during this one)
+    if (best.splits > 0)
+        best.lat = (long long)best.clusters * best.splits < (long long)num_sms * (best.tmem_cols == 256 ? 2 : 1);
     return best;
 }
 
@@ -1010,8 +1272,14 @@ cudaError_t tc_launch(const StepParams& p, const Plan& plan, const TcMaps& maps,
     args.stages = plan.stages;
     args.tmem_cols = plan.tmem_cols;
     const bool one = plan.tmem_cols == 512;   // one CTA per SM -> kMaxNG softmax groups
-    if (gpad_tc(p.G) == 4) return one ? launch_t<4, kMaxNG>(args, plan, stream) : launch_t<4, 1>(args, plan, stream);
-    return one ? launch_t<8, kMaxNG>(args, plan, stream) : launch_t<8, 1>(args, plan, stream);
+    if (plan.lat) {
+        if (gpad_tc(p.G) == 4)
+            return one ? launch_t<4, kMaxNG, true>(args, plan, stream) : launch_t<4, 1, true>(args, plan, stream);
+        return one ? launch_t<8, kMaxNG, true>(args, plan, stream) : launch_t<8, 1, true>(args, plan, stream);
+    }
+    if (gpad_tc(p.G) == 4)
+        return one ? launch_t<4, kMaxNG, false>(args, plan, stream) : launch_t<4, 1, false>(args, plan, stream);
+    return one ? launch_t<8, kMaxNG, false>(args, plan, stream) : launch_t<8, 1, false>(args, plan, stream);
 }
 
 }  // namespace lf

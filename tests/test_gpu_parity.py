@@ -342,3 +342,56 @@ def test_solo_then_split_schedule(cuda_lib):
         pytest.skip(f"planner chose no solo rounds here: {plan}")
     st = run_lockstep(cache, orc, syn, wl.steps)
     print(plan, st)
+
+
+# --- back-to-back steps with no host synchronisation (PDL overlap + speculative first tiles) ------
+
+def _enqueue_b2b(plan_of_steps, graph):
+    """plan_of_steps: list of (cache, q, kn, vn, out, slot) enqueued in order on one stream."""
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for c, q, kn, vn, out, slot in plan_of_steps:
+                c.decode_step(q, kn, vn, out, slot, stream=st)
+        g.replay()
+    else:
+        with torch.cuda.stream(st):
+            for c, q, kn, vn, out, slot in plan_of_steps:
+                c.decode_step(q, kn, vn, out, slot, stream=st)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("graph", [False, True], ids=["stream", "graph"])
+def test_back_to_back_steps_no_sync(cuda_lib, graph):
+    """Full caches stepped back to back on one stream with no host synchronisation (the bench's
+    launch pattern): step t+1 of a cache issues its first K/V tiles before its PDL wait, while step
+    t may still be writing its victim row, and patches that row after the wait.
+    Cache A (the q7 shape: 16-CTA clusters, one tile per CTA) runs 40 steps alone, then A and a
+    second cache B (2 x 8/2, N=256) are interleaved A B A B ... for 40 more steps each.  Every
+    step's out and slot, and the final caches, must equal the oracle run step by step.
+    (LF_SPEC_NOPATCH=1 — speculation without the patch — must make this test fail.)"""
+    wa = Workload("b2b_a", 1, 28, 4, 128, 2048, 2048, 0)
+    wb = Workload("b2b_b", 2, 8, 2, 128, 256, 256, 0)
+    A = setup_pair(wa, seed=5, nthreads=4)
+    B = setup_pair(wb, seed=6, nthreads=4)
+    order = [A] * 40 + [A, B] * 40
+    steps = []
+    for cache, orc, syn in order:
+        q, kn, vn = syn.step()
+        out, slot, _ = cache.new_outputs(with_scores=False)
+        steps.append((cache, orc, (q, kn, vn), out, slot))
+    _enqueue_b2b([(c, q.cuda(), kn.cuda(), vn.cuda(), out, slot) for c, _, (q, kn, vn), out, slot in steps],
+                 graph)
+    stats = Stats()
+    for cache, orc, (q, kn, vn), out, slot in steps:
+        qb, kb, vb = bits(q), bits(kn), bits(vn)
+        nv_before = orc.n_valid.copy()
+        o_ref, s_ref, sc_ref = orc.compute(qb, kb, vb, want_scores=True)
+        check_out(out.cpu().double().numpy(), o_ref, cache.out_dtype, stats)
+        chosen = accept_slots(slot.cpu().numpy(), s_ref, sc_ref, nv_before, orc.N, stats)
+        orc.apply(kb, vb, chosen)
+    assert_cache_equal(A[0], A[1])
+    assert_cache_equal(B[0], B[1])
+    print(f"back to back ({'graph' if graph else 'stream'}): A plan {A[0].plan()}, B plan {B[0].plan()}, {stats}")

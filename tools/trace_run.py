@@ -34,6 +34,15 @@ if "--flush" in sys.argv:   # cold L2 / TLB, as bench.py times L2-resident confi
 cache.decode_step(q, kn, vn, out, slot)
 torch.cuda.synchronize()
 a = tr.view(ctas, 64, 32).cpu().numpy().astype(np.int64)
+# events are SM cycles; row 0 slot 16 = entry cycles, slot 31 = entry globaltimer (ns)
+ghz = float(os.environ.get("LF_TRACE_GHZ", "1.965"))
+for c in range(ctas):
+    if a[c, 0, 16] <= 0:
+        continue
+    clk0, gt0 = a[c, 0, 16], a[c, 0, 31]
+    a[c, 0, 31] = 0
+    m = a[c] > 0
+    a[c][m] = gt0 + np.round((a[c][m] - clk0) / ghz).astype(np.int64)
 np.save(f"gpurun_out/trace_{w}.npy", a)
 used = a[:, :, 0] > 0
 t0 = a[used][:, 0].min()
