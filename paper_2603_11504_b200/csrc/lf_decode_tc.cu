@@ -615,6 +615,32 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             const uint32_t sreg = tl + par * RC;
             if (sidx == 0) LF_EVENT(ui, 0);
             if (sidx == 0) LF_EVENT(ui, 15);
+            // latency variant, one tile per CTA: its V tile lands with (or before) K, so lambda_j and
+            // the zeroing of rows past n happen while the QK MMA runs (PREADY still follows them)
+            const bool lam_first = kLat && x.ntiles == 1;
+            if (lam_first && (int)(pi % kNG) == grp) {
+                const uint32_t iv = it + 1;
+                const int st = iv % ST;
+                ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);
+                if (iv < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
+                if (q4 == 0 && lane == 0) LF_EVENT(ui, 5);
+                unsigned char* Vt = smem + so.ring + st * kStageBytes;
+                float lam = 0.f;
+                if (row < nv) {
+#pragma unroll
+                    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)));
+                } else {
+#pragma unroll
+                    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            *(uint4*)(Vt + bb * kBoxBytes + row * 128 + k * 16) = make_uint4(0, 0, 0, 0);
+                }
+                Ls[row] = lam;
+            }
             // ---- max over the unit's logits (TMEM-resident S)
             ptx::mbar_wait(BAR(KDONE + par), (ui >> 1) & 1u);
             ptx::tc_fence_after();
@@ -677,6 +703,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 }
                 const uint32_t iv = it + x.ntiles + t;
                 const int st = iv % ST;
+                if (!lam_first) {
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
                 if (iv < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                 if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 5);
@@ -698,6 +725,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                             lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)));
                 }
                 Ls[tok] = lam;
+                }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
