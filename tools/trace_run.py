@@ -81,3 +81,15 @@ if per_cta:
     print(f"r0done(u) -> start(u+1): mean {gaps.mean()/1e3:.2f} us")
     unit = np.concatenate([ev[1:, 0] - ev[:-1, 0] for ev in per_cta])
     print(f"unit period: mean {unit.mean()/1e3:.2f} us  p50 {np.median(unit)/1e3:.2f}")
+# per-CTA timeline of the first item relative to the CTA's own PDL wait (cycle-accurate: SM clock)
+rel_names = {16: "entry", 17: "csync", 18: "pdlw", 19: "pdlw(softmax)", 20: "sm_base", 21: "sm_n_loaded",
+             22: "prod_n_loaded", 24: "prod_qfree", 6: "prodQ", 7: "mmaQ", 0: "start", 15: "xsdone",
+             1: "maxdone", 5: "Vland", 2: "Vdone", 8: "xfree", 9: "ofull", 10: "ostage", 11: "pushed",
+             3: "xready", 12: "MZ", 4: "keypush", 13: "comb", 14: "r0done"}
+r0 = a[used][:, 0].astype(np.float64)
+ok0 = r0[:, 18] > 0
+print("first item, us after the CTA's own PDL wait (mean over CTAs):")
+for j, nm in rel_names.items():
+    m = ok0 & (r0[:, j] > 0)
+    if m.any():
+        print(f"  {nm:14s} {np.mean(r0[m, j] - r0[m, 18]) / 1e3:7.3f}")
