@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kNT) simt_decode_kernel(StepParams p) {
     const int s = (int)cluster.block_rank();
     const int u = blockIdx.x / S;
     const int b = u / p.Hkv, h = u % p.Hkv;
-    pdl_trigger();   // the next step's prologue may overlap this step (this kernel never speculates)
+    pdl_trigger();   // the next step's prologue may overlap this step
     pdl_wait();      // the previous step's cache writes are visible from here on
     const int n = p.n_valid[u];
     const int c0 = s * chunk;

@@ -90,9 +90,7 @@ constexpr int EMPTY = FULL + kMaxStages;
 constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kMaxNG;
 constexpr int QFULL = PFREE + kMaxNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
 constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
-constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2;
-constexpr int SPEC = XFREE + 2;         // [kMaxStages] first ring pass: speculative TMA landed / released
-constexpr int NBARS = SPEC + kMaxStages;
+constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
 static_assert(NBARS <= 48, "barrier slots");
 
 // Debug event trace (-DLF_TRACE): %clock64 at fixed points, [cta][unit % 64][32] u64; slot 31 of
@@ -169,10 +167,11 @@ __host__ __device__ inline int tc_hold(int N, int chunk, int solo_rounds) {
     return solo_rounds > 0 && Nr > chunk ? Nr : chunk;
 }
 
-// kLat: the latency variant for grids that leave SMs free (small batches): speculative first tiles,
-// per-role PDL waits after a parameter-only setup, one-round-trip operand loads, 16-lane x* / (M, Z)
-// reductions and a thread-per-element split combine.  Machine-filling grids use kLat = false, which
-// is the streaming-tuned code (measured: the latency changes cost 1-3 % there).
+// kLat: the latency variant for split plans whose grid leaves SMs free (small batches, where the
+// step is a chain of dependent latencies, not an HBM stream): one-round-trip operand loads, 16-lane
+// x* and (M, Z) reductions, a thread-per-element split combine, and lambda_j of a single-tile CTA
+// computed while its QK MMA runs.  Machine-filling and single-CTA-per-unit plans use kLat = false,
+// the streaming-tuned code (measured: the latency changes cost 1-3 % there).
 template <int GP, int kNG, bool kLat>
 __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     constexpr int kNS = 128 * kNG;          // softmax threads
@@ -224,35 +223,10 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         }
         ptx::mbar_init(BAR(OFULL), 1);
         ptx::mbar_init(BAR(OFREE), 4);
-        if constexpr (kLat)
-            for (int i = 0; i < ST; ++i) ptx::mbar_init(BAR(SPEC + i), 1);
         ptx::fence_mbar_init();
         ptx::tma_prefetch_desc(&a.tmK);
         ptx::tma_prefetch_desc(&a.tmV);
     }
-    // Speculative first tiles (same-step mode): issue the first item's first ring stages BEFORE the
-    // PDL wait, so their HBM latency overlaps the previous step's tail.  Only a unit that was full
-    // before the previous step is speculated: n never decreases between decode steps and stays N once
-    // full, so its tile count is final.  The only row of it the previous step (the one kernel that may
-    // still run: every decode kernel triggers its dependents after its own wait) can have written is
-    // wrote[u]; the producer re-reads that row after the wait and patches it into the stage before
-    // releasing the stage (FULL).  TMA completion of a speculative stage lands on SPEC.  Only grids
-    // that leave SMs free speculate (the next step's CTAs can then start during this one).
-    int nspec = 0;
-    if (kLat && tid == 0 && p.spec) {
-        const UnitInfo x = item_base(p, cid, s, C, 0);
-        if (x.valid && __ldcg(p.n_valid + x.u) >= N) {
-            const int nt = (x.c1 - x.c0 + 127) / 128;
-            nspec = min(2 * nt, ST);
-            for (int j = 0; j < nspec; ++j) {
-                const int tile = j < nt ? j : j - nt;
-                ptx::mbar_arrive_expect_tx(BAR(SPEC + j), kStageBytes);
-                ptx::tma_load_3d(ring + (uint32_t)j * kStageBytes, j < nt ? (const void*)&a.tmK : (const void*)&a.tmV,
-                                 BAR(SPEC + j), 0, x.u * N + x.c0 + tile * 128, 0);
-            }
-        }
-    }
-    if (kLat && tid == 0) *(volatile int*)(smem + so.tmem + 4) = nspec;   // read by every role after the cluster sync
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(smem + so.tmem), (uint32_t)a.tmem_cols);
     if (tid == 0) LF_EVENT(0, 16);
 #ifdef LF_TRACE
@@ -287,44 +261,18 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     ptx::cluster_sync_all();   // barriers of every rank initialised before any remote arrival
     ptx::tc_fence_after();
     if (tid == 0) LF_EVENT(0, 17);
-    // Each role runs its parameter-only setup (first item's indices and pointers) BEFORE its PDL
-    // wait, then waits: from there on the previous step's cache writes are visible.  A speculating
-    // step triggers its dependents only after its wait, so when a step starts speculating, the
-    // only step of the same cache that can still be running is the one just before it (steps of
-    // one cache share a plan, so they all speculate or none does; a chain of early-triggering
-    // steps of other caches ends at the first speculating one).
-    if constexpr (!kLat) {
-        pdl_trigger();             // the next step's prologue may overlap this step
-        pdl_wait();                // the previous step's cache writes are visible from here on
-    }
+    pdl_trigger();             // the next step's prologue may overlap this step
+    pdl_wait();                // the previous step's cache writes are visible from here on
+    if (tid == 0) LF_EVENT(0, 18);
+    if (tid == 64) LF_EVENT(0, 19);
     const uint32_t tmem = *(volatile uint32_t*)(smem + so.tmem);
-    if constexpr (kLat) nspec = *(volatile int*)(smem + so.tmem + 4);   // speculative ring indices [0, nspec)
-    const UnitInfo x0 = item_base(p, cid, s, C, 0);
-    auto dep_wait = [&]() {
-        if constexpr (kLat) {
-            // the empty asm statements consume the setup values, so they are computed (and the kernel
-            // parameters they read are in the constant cache) before the wait -- nvcc otherwise sinks them
-            asm volatile("" ::"r"(x0.u), "r"(x0.b), "r"(x0.h), "r"(x0.c0), "r"(x0.c1), "r"((int)x0.valid));
-            asm volatile("" ::"l"(p.q), "l"(p.k_new), "l"(p.v_new), "l"(p.n_valid), "l"(p.out), "l"(p.wrote));
-            asm volatile("" ::"r"(p.Hq), "r"(p.N), "r"(p.chunk), "r"(p.out_f32), "f"(p.scale_log2), "l"(p.scores));
-            if (p.spec) {   // speculating steps trigger after the wait (at most one earlier step runs)
-                pdl_wait();
-                pdl_trigger();
-            } else {
-                pdl_trigger();
-                pdl_wait();
-            }
-        }
-    };
 
     if (warp == 0) {
         // ------------------------------ producer -------------------------------------------------
         if constexpr (kLat) {
             uint32_t it = 0, qi = 0;
-            dep_wait();
-            if (lane == 0) LF_EVENT(0, 18);
             for (int i = 0;; ++i, ++qi) {
-                // every global read of the item goes out at once (Q rows, fill state, last written slot):
+                // every global read of the item goes out at once (Q rows, fill state):
                 // one L2 round trip instead of a chain of them before the first MMA
                 UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
@@ -332,10 +280,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const int qb = qi & 1;
                 const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
                 uint4 qv[4];
-    #pragma unroll
+#pragma unroll
                 for (int k = 0; k < 4; ++k) qv[k] = lane + 32 * k < G * 16 ? __ldg(qg + lane + 32 * k) : make_uint4(0, 0, 0, 0);
-                const bool spec_item = i == 0 && nspec > 0;
-                const int ws = spec_item ? __ldcg(p.wrote + u) : -1;
                 x.n = __ldcg(p.n_valid + u);
                 x.nv = max(0, min(x.c1, x.n) - x.c0);
                 x.ntiles = (x.nv + 127) / 128;
@@ -354,34 +300,13 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
                     ++it;
                 };
-                int first = 0;
-                if (spec_item) {
-                    // speculative stages: patch the row the previous step wrote (if it lies in one), release
-                    for (int j = 0; j < nspec; ++j) {
-                        const int tile = j < x.ntiles ? j : j - x.ntiles;
-                        const int r = ws - x.c0 - tile * 128;
-                        if (r >= 0 && r < 128 && p.spec == 1) {   // warp-uniform (spec 2: debug, no patch)
-                            const uint16_t* src = (j < x.ntiles ? p.K : p.V) + ((size_t)u * N + ws) * 128;
-                            const uint4 w = lane < 16 ? __ldcg((const uint4*)src + lane) : make_uint4(0, 0, 0, 0);
-                            ptx::mbar_wait(BAR(SPEC + j), 0);   // landed: the TMA must not overwrite the patch
-                            if (lane < 16)
-                                *(uint4*)(smem + so.ring + j * kStageBytes + (lane >> 3) * kBoxBytes + r * 128 +
-                                          (((lane & 7) ^ (r & 7)) << 4)) = w;
-                            ptx::fence_proxy_async_smem();
-                            __syncwarp();
-                        }
-                        if (lane == 0) ptx::mbar_arrive(BAR(FULL + j));
-                    }
-                    it = (uint32_t)nspec;
-                    first = nspec;
-                }
                 if (lane == 0)
-                    for (int i = first; i < pre; ++i) issue(i);
+                    for (int i = 0; i < pre; ++i) issue(i);
                 ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
                 if (lane == 0 && i == 0) LF_EVENT(0, 24);
                 // Q^T rows g < G (K-major SW128): 16 B chunk c of row g at chunk (c%8) ^ g of box c/8
                 unsigned char* qd = smem + so.q + qb * 4096;
-    #pragma unroll
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int e = lane + 32 * k, g = e >> 4, c = e & 15;
                     if (e < G * 16) *(uint4*)(qd + (c >> 3) * 1024 + g * 128 + (((c & 7) ^ g) << 4)) = qv[k];
@@ -438,7 +363,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------------------------
-        dep_wait();
         if (lane == 0) {
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
@@ -457,7 +381,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it) {                  // S^T = K_tile . Q^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    if (it < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                     LF_TILE_EVENT(ui, 32, t);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
@@ -475,7 +398,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    if (it < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                     const int pb = pi % kNG;
                     ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
                     ptx::tc_fence_after();
@@ -548,8 +470,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             return best;
         };
         uint32_t it = 0, pi = 0, ui = 0, xi = 0;
-        dep_wait();
-        if (sidx == 0) LF_EVENT(0, 19);
         for (int i = 0;; ++i, ++ui) {
             UnitInfo x;
             uint4* kvn = (uint4*)(smem + so.kvn);
@@ -578,12 +498,12 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 if (sidx < 128) {
                     float acc = 0.f;
                     const uint32_t qw[4] = {xq.x, xq.y, xq.z, xq.w}, kw[4] = {xk.x, xk.y, xk.z, xk.w};
-    #pragma unroll
+#pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         acc = fmaf(__uint_as_float(qw[k] << 16), __uint_as_float(kw[k] << 16), acc);
                         acc = fmaf(__uint_as_float(qw[k] & 0xffff0000u), __uint_as_float(kw[k] & 0xffff0000u), acc);
                     }
-    #pragma unroll
+#pragma unroll
                     for (int off = 8; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (xch == 0 && xg < G) xs[xg] = p.deferred ? -INFINITY : acc * sl2;
                 }
@@ -602,9 +522,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     const uint16_t* qg = p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + g) * 128;
                     const uint16_t* kn = p.k_new + (size_t)u * 128;
                     float acc = 0.f;
-    #pragma unroll
+#pragma unroll
                     for (int l = lane; l < 128; l += 32) acc = fmaf(bf16_to_f32(qg[l]), bf16_to_f32(kn[l]), acc);
-    #pragma unroll
+#pragma unroll
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (lane == 0) xs[g] = p.deferred ? -INFINITY : acc * sl2;
                 }
@@ -622,7 +542,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const uint32_t iv = it + 1;
                 const int st = iv % ST;
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);
-                if (iv < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                 if (q4 == 0 && lane == 0) LF_EVENT(ui, 5);
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 float lam = 0.f;
@@ -705,7 +624,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const int st = iv % ST;
                 if (!lam_first) {
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
-                if (iv < (uint32_t)nspec) ptx::mbar_wait(BAR(SPEC + st), 0);
                 if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 5);
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
@@ -806,7 +724,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int sl = x.n < N ? x.n : (int)(kb & 0xffffffffull);
                         *s_slot = sl;
                         p.slot[u] = sl;
-                        if constexpr (kLat) p.wrote[u] = sl;
                         if (x.n < N) p.n_valid[u] = x.n + 1;
                     }
                 }
@@ -890,11 +807,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     }
                     const float xsg = g < G ? xs[g] : -INFINITY;
                     float M = fmaxf(xsg, mr);
-    #pragma unroll
+#pragma unroll
                     for (int off = 8; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
                     const float f = r < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
                     float Z = zr * f;
-    #pragma unroll
+#pragma unroll
                     for (int off = 8; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
                     const float fn = ptx::ex2_approx(xsg - M);
                     Z += fn;
@@ -917,11 +834,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         zr = xc->mz[lane][g][1];
                     }
                     float M = fmaxf(xs[g], mr);
-    #pragma unroll
+#pragma unroll
                     for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
                     const float f = lane < S ? ptx::ex2_approx(mr - M) : 0.f;   // same factors as P and o
                     float Z = zr * f;
-    #pragma unroll
+#pragma unroll
                     for (int off = 16; off > 0; off >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, off);
                     Z += ptx::ex2_approx(xs[g] - M);
                     if (lane < S) fr[g * 16 + lane] = f;
@@ -962,7 +879,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int i4 = i4_0 + e;
                         const int g = i4 >> 5, l = (i4 & 31) * 4;
                         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    #pragma unroll 4
+#pragma unroll 4
                         for (int r = 0; r < S; ++r) {
                             const float f = fr[g * 16 + r];
                             const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
@@ -1047,7 +964,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int sl = x.n < N ? x.n : (int)(mk & 0xffffffffull);
                         *s_slot = sl;
                         p.slot[u] = sl;
-                        if constexpr (kLat) p.wrote[u] = sl;
                         if (x.n < N) p.n_valid[u] = x.n + 1;
                     }
                 }
@@ -1279,8 +1195,9 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         }
         if (split_tokens > 0) break;
     }
-    // latency variant when the grid leaves SMs free (the next step's CTAs can start during this one)
-    if (best.splits > 0)
+    // latency variant: split plans whose grid leaves SMs free (measured: it helps the split
+    // exchange chain of small batches; solo and machine-filling plans stay on the streaming code)
+    if (best.splits > 1)
         best.lat = (long long)best.clusters * best.splits < (long long)num_sms * (best.tmem_cols == 256 ? 2 : 1);
     return best;
 }

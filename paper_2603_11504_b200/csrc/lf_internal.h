@@ -23,10 +23,6 @@ struct StepParams {
     int32_t exclude_newest; // deferred mode: the slot just written is not a candidate
     int32_t* pend;          // deferred mode: int32 [B][Hkv] slot covered at the next step
     const int32_t* written; // deferred mode: int32 [B][Hkv] slot the current token was written to
-    int32_t* wrote;         // int32 [B][Hkv] (cache-internal): slot this step's k*, v* went to (-1: none)
-    int32_t spec;           // 1: tcgen05 kernel may issue its first K/V tiles before the PDL wait and
-                            //    patch the row the previous step wrote (same-step mode only);
-                            //    2: debug negative control, speculate without the patch (wrong results)
     int32_t B, Hq, Hkv, G, d, N;
     int32_t out_f32;        // 1: fp32 out, 0: bf16 out
     float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip
@@ -49,7 +45,7 @@ struct Plan {
     int32_t stages;   // TMA ring depth (tcgen05 kernel)
     int32_t tmem_cols;  // TMEM columns per CTA (tcgen05 kernel)
     int32_t solo_rounds;  // tcgen05: rounds of whole units per CTA before the split tail
-    int32_t lat;          // tcgen05: 1 = latency variant (the grid leaves SMs free), 0 = streaming
+    int32_t lat;          // tcgen05: 1 = latency variant (split plan, grid leaves SMs free), 0 = streaming
 };
 
 // deferred mode pre-pass: the current token covers pend[u] (or is appended) before attention

@@ -35,7 +35,7 @@ lf_status cuda_fail(cudaError_t e, const char* what) {
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
-    size_t k_off, v_off, nv_off, pd_off, wr_off, sq_off, sk_off, sv_off, so_off, ss_off, total;
+    size_t k_off, v_off, nv_off, pd_off, sq_off, sk_off, sv_off, so_off, ss_off, total;
 };
 
 Layout layout_of(const lf_cache_config& c) {
@@ -46,7 +46,6 @@ Layout layout_of(const lf_cache_config& c) {
     L.v_off = off; off = align_up(off + kv, 256);
     L.nv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
     L.pd_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
-    L.wr_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * 4, 256);
     L.sq_off = off; off = align_up(off + (size_t)c.batch * c.num_q_heads * c.head_dim * 2, 256);
     L.sk_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
     L.sv_off = off; off = align_up(off + (size_t)c.batch * c.num_kv_heads * c.head_dim * 2, 256);
@@ -275,7 +274,6 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
     // all slots invalid; zero-filled storage; no pending victim (-1)
     e = cudaMemset(c->slab, 0, c->L.total);
     if (e == cudaSuccess) e = cudaMemset((char*)c->slab + c->L.pd_off, 0xff, (size_t)cfg->batch * cfg->num_kv_heads * 4);
-    if (e == cudaSuccess) e = cudaMemset((char*)c->slab + c->L.wr_off, 0xff, (size_t)cfg->batch * cfg->num_kv_heads * 4);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -482,14 +480,6 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.exclude_newest = g.mode == LF_EVICT_DEFERRED_EXCLUDE_NEWEST;
     p.pend = (int32_t*)(base + c->L.pd_off);
     p.written = slot;
-    p.wrote = (int32_t*)(base + c->L.wr_off);
-    {
-        static const bool no_spec = getenv("LF_NO_SPEC") != nullptr;          // A/B switch
-        static const bool no_patch = getenv("LF_SPEC_NOPATCH") != nullptr;   // negative control (wrong results)
-        // speculate only in the latency variant (the grid leaves room for the next step's CTAs)
-        const bool room = c->plan.kernel == LF_KERNEL_TCGEN05 && c->plan.lat;
-        p.spec = p.deferred || no_spec || !room ? 0 : no_patch ? 2 : 1;
-    }
     p.B = g.batch;
     p.Hq = g.num_q_heads;
     p.Hkv = g.num_kv_heads;

@@ -366,12 +366,12 @@ def _enqueue_b2b(plan_of_steps, graph):
 @pytest.mark.parametrize("graph", [False, True], ids=["stream", "graph"])
 def test_back_to_back_steps_no_sync(cuda_lib, graph):
     """Full caches stepped back to back on one stream with no host synchronisation (the bench's
-    launch pattern): step t+1 of a cache issues its first K/V tiles before its PDL wait, while step
-    t may still be writing its victim row, and patches that row after the wait.
-    Cache A (the q7 shape: 16-CTA clusters, one tile per CTA) runs 40 steps alone, then A and a
-    second cache B (2 x 8/2, N=256) are interleaved A B A B ... for 40 more steps each.  Every
-    step's out and slot, and the final caches, must equal the oracle run step by step.
-    (LF_SPEC_NOPATCH=1 — speculation without the patch — must make this test fail.)"""
+    launch pattern): with programmatic dependent launch, step t+1's prologue runs while step t is
+    still writing its victim row, and its first dependent read must come after its PDL wait.
+    Cache A (the q7 shape: 16-CTA clusters, one tile per CTA, the latency variant) runs 40 steps
+    alone, then A and a second cache B (2 x 8/2, N=256, streaming variant) are interleaved
+    A B A B ... for 40 more steps each.  Every step's out and slot, and the final caches, must
+    equal the oracle run step by step."""
     wa = Workload("b2b_a", 1, 28, 4, 128, 2048, 2048, 0)
     wb = Workload("b2b_b", 2, 8, 2, 128, 256, 256, 0)
     A = setup_pair(wa, seed=5, nthreads=4)
