@@ -11,7 +11,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <new>
+#include <utility>
+#include <vector>
 
 #include "lf_internal.h"
 
@@ -170,7 +173,36 @@ lf_status make_plan(lf_cache* c) {
     if (want_tc) {
         if (!lf::tc_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "tcgen05 kernel not built for G=%d d=%d", G, g.head_dim);
-        c->plan = lf::tc_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+        // The plan depends only on the shape and the device (occupancy queries: ~1 ms per plan), and
+        // a model creates one cache per layer with the same shape: memoise it per process.
+        struct Key {
+            int dev, units, G, d, N, split, sms;
+            bool operator==(const Key& o) const {
+                return dev == o.dev && units == o.units && G == o.G && d == o.d && N == o.N && split == o.split &&
+                       sms == o.sms;
+            }
+        };
+        static std::mutex mu;
+        static std::vector<std::pair<Key, lf::Plan>> memo;
+        const Key k{c->device, units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms};
+        const bool forced = getenv("LF_FORCE_PLAN") != nullptr || getenv("LF_DEBUG_PLAN") != nullptr;
+        bool hit = false;
+        {
+            std::lock_guard<std::mutex> lock(mu);
+            for (const auto& e : memo)
+                if (!forced && e.first == k) {
+                    c->plan = e.second;
+                    hit = true;
+                    break;
+                }
+        }
+        if (!hit) {
+            c->plan = lf::tc_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+            if (!forced && c->plan.splits > 0) {
+                std::lock_guard<std::mutex> lock(mu);
+                memo.push_back({k, c->plan});
+            }
+        }
     } else {
         if (!lf::simt_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "CUDA-core kernel not built for G=%d d=%d", G, g.head_dim);

@@ -5,6 +5,7 @@ import argparse
 import json
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -24,6 +25,8 @@ f = open(args.out, "w")
 for N in map(int, args.budgets.split(",")):
     for B in map(int, args.batches.split(",")):
         wl = sweep_workload(B, N)
+        t0 = time.time()
+        tl = {}
         cache = Cache(B, wl.Hq, wl.Hkv, wl.d, N, out_dtype="bf16")
         K, V, nv = cache.views()
         k0, v0 = random_cache(B, wl.Hkv, N, wl.d, device="cuda")
@@ -36,6 +39,7 @@ for N in map(int, args.budgets.split(",")):
         for i in range(5):
             cache.decode_step(*pool[i % 4], out, slot, stream=st)
         torch.cuda.synchronize()
+        tl["setup"] = time.time() - t0
         flush = g = None
         cb = cache_bytes_per_gpu(wl, B)
         L = layers_for(cb)
@@ -45,6 +49,7 @@ for N in map(int, args.budgets.split(",")):
             K2, V2, nv2 = c2.views()
             K2.copy_(K); V2.copy_(V); nv2.copy_(nv)
             layers.append(c2)
+        tl["layers"] = time.time() - t0
         steps = max(3, min(args.steps, 2000 // max(L, 1)))   # bounded graph size (<= ~2000 launches)
         if L == 0:
             flush = torch.zeros(128 << 20, dtype=torch.float32, device="cuda")
@@ -63,7 +68,9 @@ for N in map(int, args.budgets.split(",")):
             def run(i):
                 with torch.cuda.stream(st):
                     g.replay()
+        tl["graph"] = time.time() - t0
         us = timed_steps(run, steps * max(L, 1), st, flush) * 1e3
+        tl["timed"] = time.time() - t0
         alg = alg_bytes_per_step(wl, B, 2)
         rec = {"B": B, "N": N, "latency_us": us, "tokens_per_s": B / (us * 1e-6), "alg_bytes": alg,
                "GBps": alg / (us * 1e-6) / 1e9, "frac_measured_peak": alg / (us * 1e-6) / 1e9 / peak,
@@ -75,3 +82,5 @@ for N in map(int, args.budgets.split(",")):
             c.close()
         del cache, K, V, nv, pool, out, slot, flush, g, layers
         torch.cuda.empty_cache()
+        tl["closed"] = time.time() - t0
+        print("phase times (s, cumulative):", {k: round(v, 2) for k, v in tl.items()}, file=sys.stderr, flush=True)
