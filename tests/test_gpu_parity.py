@@ -62,6 +62,7 @@ SHAPES = [  # (B, Hq, Hkv, d, N, prefill, steps, split_tokens)
     (48, 32, 8, 128, 384, 370, 14, 128),  # 384 units x 3-CTA clusters, fill -> evict
     (2, 3, 3, 128, 300, 290, 14, 128),  # G=1 at d=128 (tcgen05 with one live head), 3 splits
     (5, 4, 4, 128, 640, 630, 14, 0),    # G=1, solo units
+    (1, 10, 2, 128, 1100, 1090, 14, 384),  # G=5, 3-tile CTAs + ragged last chunk (latency variant)
 ]
 
 
