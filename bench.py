@@ -11,7 +11,7 @@ hot path (logits, softmax, PV, LongFlowScore, argmin, in-place eviction) on a FU
 so every step evicts.  value = tokens/s summed over ranks (one token per sequence per step).
 Inputs of 8 pre-generated steps live in HBM; the cache (8.6 GB per GPU for `r`) is far larger
 than L2, so no L2 flush is needed between steps.  Caches below FLUSH_BELOW bytes per GPU would sit in
-the 126 MB L2 across steps.  For them the bench cycles L = ceil(4 x L2 / cache)
+the 126 MB L2 across steps.  For them the bench cycles L = ceil(8 x L2 / cache)
 layer caches of the same shape -- like the L layers of a model, each layer's cache is cold in L2 when
 its step runs -- in one CUDA graph of K x L back-to-back steps; ms_per_step = time / (K x L).  When L
 would exceed MAX_LAYERS (`tiny`), every timed step is instead preceded by an untimed 512 MB read (L2
@@ -216,16 +216,17 @@ def run_reference(args, wl, B_total):
     return 0
 
 
-FLUSH_BELOW = 512 << 20   # cache bytes per GPU under which the cache would stay L2-resident across steps
+FLUSH_BELOW = 1 << 30     # cache bytes per GPU under which part of the cache could stay L2-resident across steps
+CYCLE_FACTOR = 8          # cycled layer caches total >= 8 x L2 (4 x left part of a 268 MB cache in L2)
 L2_BYTES = 126 << 20
 MAX_LAYERS = 256
 
 
 def layers_for(cb):
-    """Layer caches to cycle so that their total is >= 4 x L2 (0: use the flush method)."""
+    """Layer caches to cycle so that their total is >= 8 x L2 (0: use the flush method)."""
     if cb >= FLUSH_BELOW:
         return 1
-    L = -(-4 * L2_BYTES // max(cb, 1))
+    L = -(-CYCLE_FACTOR * L2_BYTES // max(cb, 1))
     return L if L <= MAX_LAYERS else 0
 
 
@@ -238,7 +239,7 @@ def l2_note(cb):
         return "inputs larger than L2 (cache {:.2f} GB per GPU > 126 MB L2)".format(cb / 1e9)
     L = layers_for(cb)
     if L:
-        return ("{} layer caches of {:.1f} MB cycled back to back in one CUDA graph ({:.0f} MB > 4 x L2): "
+        return ("{} layer caches of {:.1f} MB cycled back to back in one CUDA graph ({:.0f} MB > 8 x L2): "
                 "each step's cache is cold in L2, as in an L-layer model".format(L, cb / 1e6, L * cb / 1e6))
     return ("L2 flushed before every timed step (512 MB read, untimed; cache {:.1f} MB per GPU); "
             "per-step CUDA events, no graph".format(cb / 1e6))

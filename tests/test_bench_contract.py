@@ -52,7 +52,7 @@ def test_l2_methods():
     assert big > bench.FLUSH_BELOW and bench.layers_for(big) == 1
     q7 = bench.cache_bytes_per_gpu(CONFIGS["q7"], 1)
     L = bench.layers_for(q7)
-    assert 1 < L <= bench.MAX_LAYERS and L * q7 >= 4 * bench.L2_BYTES
+    assert 1 < L <= bench.MAX_LAYERS and L * q7 >= bench.CYCLE_FACTOR * bench.L2_BYTES
     assert bench.layers_for(bench.cache_bytes_per_gpu(CONFIGS["tiny"], 1)) == 0
     assert "flushed" in bench.l2_note(bench.cache_bytes_per_gpu(CONFIGS["tiny"], 1))
     assert "layer caches" in bench.l2_note(q7) and "larger than L2" in bench.l2_note(big)
