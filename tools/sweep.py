@@ -1,6 +1,6 @@
 """BASELINE configs[4]: budget sweep 512-16384 x batch 1-512 at fixed 80 % compression (32/8 GQA, d=128):
 latency and HBM GB/s per point (full cache, every step evicts), one JSON line per point.
-usage: python tools/sweep.py [--out gpurun_out/sweep.jsonl] [--steps 20]"""
+usage: python tools/sweep.py [--out gpurun_out/sweep.jsonl] [--steps 20] [--per-row 300]"""
 import argparse
 import json
 import os
@@ -19,7 +19,25 @@ ap.add_argument("--out", default="gpurun_out/sweep.jsonl")
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--budgets", default="512,1024,2048,4096,8192,16384")
 ap.add_argument("--batches", default="1,2,4,8,16,32,64,128,256,512")
+ap.add_argument("--per-row", type=float, default=0.0,
+                help="run each budget row in its own process with this timeout (s); a stalled row is "
+                     "reported and skipped (DESIGN.md section 14)")
 args = ap.parse_args()
+if args.per_row > 0:
+    import subprocess
+    with open(args.out, "w") as f:
+        for N in args.budgets.split(","):
+            tmp = args.out + f".row{N}"
+            cmd = [sys.executable, os.path.abspath(__file__), "--out", tmp, "--steps", str(args.steps),
+                   "--budgets", N, "--batches", args.batches]
+            try:
+                subprocess.run(cmd, timeout=args.per_row, check=False)
+            except subprocess.TimeoutExpired:
+                print(f"row N={N}: timed out after {args.per_row:.0f} s", file=sys.stderr, flush=True)
+            if os.path.exists(tmp):
+                f.write(open(tmp).read())
+                os.remove(tmp)
+    sys.exit(0)
 peak, _ = peaks()
 f = open(args.out, "w")
 for N in map(int, args.budgets.split(",")):
