@@ -1159,7 +1159,8 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                 // fit (2 x 93 KB SMEM, 2 x 30K registers, 2 x 256 TMEM columns); measured on B200 the
                 // two co-reside (e.g. 512 x N=512: 200 -> 166 us), so the k = 2 grid is doubled.  The
                 // persistent loop is correct either way (no cross-cluster dependency).
-                if (k == 2) C *= 2;
+                static const bool no_double = getenv("LF_NO_K2_DOUBLE") != nullptr;   // stall probe (DESIGN 14)
+                if (k == 2 && !no_double) C *= 2;
                 if (C <= 0) continue;
                 if (const char* f = getenv("LF_FORCE_PLAN")) {   // debug: "S,k,solo"
                     int fs = 0, fk = 0, fo = -1;
