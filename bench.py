@@ -142,10 +142,10 @@ class OracleSample:
     sequences with all their kv heads, threads = host cores.  Cost is exactly linear in units,
     so a per-step time scales to the full batch by (B_total / Bs)."""
 
-    def __init__(self, wl: Workload, Bs: int, seed: int = 0):
+    def __init__(self, wl: Workload, Bs: int, seed: int = 0, nthreads: int = 0):
         import oracle
         self.wl, self.Bs = wl, Bs
-        self.cores = os.cpu_count() or 1
+        self.cores = nthreads or os.cpu_count() or 1
         self.orc = oracle.OracleCache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, nthreads=self.cores)
         k, v = random_cache(Bs, wl.Hkv, wl.N, wl.d, seed=seed)
         self.orc.K[...] = bits(k)
@@ -163,17 +163,29 @@ class OracleSample:
         return time.perf_counter() - t0
 
 
-def oracle_sample(wl: Workload, B_total: int, seconds_per_step: float, seed: int = 0) -> OracleSample:
+def oracle_sample(wl: Workload, B_total: int, seconds_per_step: float, seed: int = 0,
+                  nthreads: int = 0) -> OracleSample:
     """Grows the sample (x4 sequences at a time, capped at the batch) until one oracle step over
     it takes about `seconds_per_step`."""
     Bs = 1
-    smp = OracleSample(wl, Bs, seed)
+    smp = OracleSample(wl, Bs, seed, nthreads)
     t = smp.step()
     while t < seconds_per_step / 2 and Bs < B_total:
         Bs = min(B_total, max(Bs + 1, int(Bs * min(4.0, seconds_per_step / max(t, 1e-6)))))
-        smp = OracleSample(wl, Bs, seed)
+        smp = OracleSample(wl, Bs, seed, nthreads)
         t = smp.step()
     return smp
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def describe(smp: OracleSample, steps: int, B_total: int) -> str:
@@ -182,12 +194,26 @@ def describe(smp: OracleSample, steps: int, B_total: int) -> str:
             f"linearly by {B_total}/{smp.Bs} units to the whole batch")
 
 
-def oracle_rate(wl: Workload, B_total: int, seconds: float = 12.0, seed: int = 0):
-    """cpu_baseline leg: ~`seconds` of oracle time.  Returns (tokens/s, cores, sample, s/step)."""
-    smp = oracle_sample(wl, B_total, seconds / 4, seed)
-    ts = [smp.step() for _ in range(3)]
+def timed_oracle(wl: Workload, B_total: int, seconds: float, seed: int, nthreads: int):
+    """max(3 steps, `seconds`) of oracle steps on a sample sized to ~seconds/4 per step
+    (BASELINE.md section 4).  Returns (tokens/s, threads, sample description, s/step)."""
+    smp = oracle_sample(wl, B_total, seconds / 4, seed, nthreads)
+    ts, t0 = [], time.perf_counter()
+    while len(ts) < 3 or time.perf_counter() - t0 < seconds:
+        ts.append(smp.step())
     sps = float(np.median(ts)) * B_total / smp.Bs
-    return B_total / sps, smp.cores, describe(smp, 3, B_total), sps
+    return B_total / sps, smp.cores, describe(smp, len(ts), B_total), sps
+
+
+def oracle_rate(wl: Workload, B_total: int, seconds: float = 10.0, seed: int = 0) -> dict:
+    """cpu_baseline leg: the oracle on all host cores and on one thread, each for max(3 steps,
+    `seconds`), extrapolated linearly in units to the whole batch."""
+    v, cores, desc, sps = timed_oracle(wl, B_total, seconds, seed, 0)
+    v1, _, desc1, sps1 = timed_oracle(wl, B_total, seconds, seed, 1)
+    return {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc,
+            "ms_per_step": sps * 1e3,
+            "one_thread": {"value": v1, "unit": "tokens/s", "ms_per_step": sps1 * 1e3, "sample": desc1},
+            "cpu_model": cpu_model()}
 
 
 def run_reference(args, wl, B_total):
@@ -278,7 +304,10 @@ def config_of(args, wl, B_total, plan):
          "layer_caches": max(layers_for(cache_bytes_per_gpu(wl, B_total // max(args.gpus, 1))), 1)}
     if plan:
         c.update({"kernel": plan["kernel"], "splits": plan["splits"], "split_tokens": plan["split_tokens"],
-                  "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1})
+                  "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1,
+                  "latency_variant": plan.get("latency_variant", 0)})
+        if args.gpus > 1 and args.scaling == "strong":
+            c["shard_plan"] = "plan of the global batch (plan_batch), bit-identical to one GPU"
     if getattr(args, "mode", "same_step") != "same_step":
         c["mode"] = args.mode
     return c
@@ -295,8 +324,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="r", help="tiny | q7 | q3 | r | f1 | sweep_b<B>_n<N>")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="weak: every GPU holds the workload's batch; strong: the batch is split")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="strong (BASELINE configs[3]): the workload's batch is sharded by sequence across the "
+                         "GPUs, each shard computed exactly as on one GPU (plan_batch); weak: every GPU holds "
+                         "the workload's whole batch")
+    ap.add_argument("--ctas-per-sm", type=int, default=0, choices=[0, 1, 2], help="plan override (0 = auto)")
+    ap.add_argument("--solo", default="auto", choices=["auto", "on", "off"], help="plan override")
+    ap.add_argument("--latency-variant", default="auto", choices=["auto", "on", "off"], help="plan override")
     ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
     ap.add_argument("--split-tokens", type=int, default=0)
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
@@ -305,6 +339,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch steps directly instead of a CUDA graph")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="cpu_baseline: each of the all-cores and one-thread oracle timings runs max(3 steps, this)")
     ap.add_argument("--seed", type=int, default=0)
     args = ap.parse_args()
     if args.warmup < 3:
@@ -340,8 +376,14 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         pg = dist
 
-    cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
-                  split_tokens=args.split_tokens, device=local, mode=args.mode)
+    onoff = {"auto": None, "on": True, "off": False}
+    # strong scaling: this rank's shard is computed with the plan of the whole batch (bit-identical
+    # to the one-GPU run); weak scaling: every rank holds a whole problem
+    shard_kw = dict(plan_batch=B_total, seq_offset=b0) if args.scaling == "strong" and args.gpus > 1 else {}
+    cache_kw = dict(out_dtype=args.out_dtype, kernel=args.kernel, split_tokens=args.split_tokens, device=local,
+                    mode=args.mode, ctas_per_sm=args.ctas_per_sm, solo=onoff[args.solo],
+                    latency_variant=onoff[args.latency_variant], **shard_kw)
+    cache = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, **cache_kw)
     plan = cache.plan()
     K, V, nv = cache.views()
     k0, v0 = random_cache(B, wl.Hkv, wl.N, wl.d, seed=args.seed, device=dev, b0=b0)
@@ -359,8 +401,7 @@ def main():
     n_layers = layers_for(cache_bytes_per_gpu(wl, B))
     layers = [cache]
     for _ in range(1, max(n_layers, 1)):
-        c2 = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=args.out_dtype, kernel=args.kernel,
-                   split_tokens=args.split_tokens, device=local, mode=args.mode)
+        c2 = Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, **cache_kw)
         K2, V2, nv2 = c2.views()
         K2.copy_(K)
         V2.copy_(V)
@@ -481,9 +522,8 @@ def main():
     }
     if gather:
         line["nccl_gather_out_slot"] = gather
-    if rank == 0 and args.gpus == 1 and not args.no_cpu_baseline:
-        v, cores, desc, sps = oracle_rate(wl, B_total, seconds=args.ref_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": "tokens/s", "cores": cores, "kind": "oracle", "sample": desc}
+    if rank == 0 and not args.no_cpu_baseline:   # rank 0 only; the other ranks wait at the barrier below
+        line["cpu_baseline"] = oracle_rate(wl, B_total, seconds=args.cpu_seconds)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if pg:

@@ -79,6 +79,21 @@ typedef struct {
     int32_t mode;          /* lf_evict_mode                                                     */
     int32_t kernel;        /* lf_kernel                                                         */
     int32_t split_tokens;  /* tokens per split-KV CTA (multiple of 128), 0 = automatic plan     */
+    /* Sharding by sequence ("beneficial in distributed systems").  The
+     * split plan fixes each unit's reduction order (how its tokens are divided among CTAs and in
+     * which order the partial (m, Z, o) are merged), so it is computed for the GLOBAL problem: a
+     * rank holding sequences [seq_offset, seq_offset + batch) of a global batch passes
+     * plan_batch = the global batch, and every unit is computed exactly as the one-GPU cache of
+     * plan_batch sequences computes it (bit-identical out, scores and slot).  0 = this cache is
+     * the whole problem (plan_batch = batch, seq_offset = 0). */
+    int32_t plan_batch;    /* 0, or >= seq_offset + batch                                        */
+    int32_t seq_offset;    /* first sequence of this cache in the global batch (0 if plan_batch == 0) */
+    /* Plan overrides (tests and measurements; 0 = automatic).  They change which CTAs compute a
+     * unit, never what is computed. */
+    int32_t ctas_per_sm;      /* tcgen05: 1 (three softmax groups, 512 TMEM columns) or 2 (one group, 256) */
+    int32_t solo;             /* tcgen05: 1 = every unit split across its cluster, 2 = rounds of whole units
+                                 per CTA before the split tail (needs splits > 1 and budget <= 4096)      */
+    int32_t latency_variant;  /* tcgen05 split plans: 1 = streaming code, 2 = latency variant           */
 } lf_cache_config;
 
 /* Bytes of the device slab for `cfg` (K, V, per-unit valid counts, staging for the host
@@ -161,9 +176,11 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits,
 
 /* More of the plan: persistent clusters in the grid (0 = one cluster per unit), TMA ring stages,
  * TMEM columns per CTA (512 = one CTA per SM, 256 = two, 0 = CUDA-core kernel), SMEM bytes per CTA,
- * rounds of whole units per CTA before the units split across the cluster.  NULL outputs are skipped. */
+ * rounds of whole units per CTA before the units split across the cluster (of the plan_batch
+ * problem), and whether split units use the latency variant (1) or the streaming code (0).  NULL
+ * outputs are skipped. */
 lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
-                               int32_t* smem_bytes, int32_t* solo_rounds);
+                               int32_t* smem_bytes, int32_t* solo_rounds, int32_t* latency_variant);
 
 /* Deferred modes: device view of int32 [B][Hkv], the slot the next step's token will cover
  * (-1 = none yet).  In deferred modes lf_decode_step's `slot` returns where the current token

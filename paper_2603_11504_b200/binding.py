@@ -39,7 +39,8 @@ class CacheConfig(ctypes.Structure):
     _fields_ = [("batch", ctypes.c_int32), ("num_q_heads", ctypes.c_int32), ("num_kv_heads", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("budget", ctypes.c_int32), ("out_dtype", ctypes.c_int32),
                 ("softmax_scale", ctypes.c_float), ("mode", ctypes.c_int32), ("kernel", ctypes.c_int32),
-                ("split_tokens", ctypes.c_int32)]
+                ("split_tokens", ctypes.c_int32), ("plan_batch", ctypes.c_int32), ("seq_offset", ctypes.c_int32),
+                ("ctas_per_sm", ctypes.c_int32), ("solo", ctypes.c_int32), ("latency_variant", ctypes.c_int32)]
 
 
 _lib = None
@@ -63,7 +64,7 @@ def load(path: str = os.environ.get("LF_LIB", LIB_PATH)):
     lib.lf_decode_step_host.argtypes = [P, P, P, P, P, P, P]
     lib.lf_cache_views.argtypes = [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]
     lib.lf_cache_plan.argtypes = [P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32)]
-    lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 5
+    lib.lf_cache_plan_detail.argtypes = [P] + [ctypes.POINTER(i32)] * 6
     lib.lf_cache_plan_detail.restype = ctypes.c_int
     lib.lf_snapkv_workspace_bytes.argtypes = [P, i32, i32, ctypes.POINTER(sz)]
     lib.lf_snapkv_workspace_bytes.restype = ctypes.c_int
@@ -110,10 +111,17 @@ def _stream(stream):
     return int(stream)
 
 
+# plan overrides (lf_cache_config): None/"auto" = automatic
+_SOLO = {None: 0, "auto": 0, False: 1, True: 2}
+_LAT = {None: 0, "auto": 0, False: 1, True: 2}
+
+
 def make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32", softmax_scale=0.0,
-                kernel="auto", split_tokens=0, mode="same_step") -> CacheConfig:
+                kernel="auto", split_tokens=0, mode="same_step", plan_batch=0, seq_offset=0, ctas_per_sm=0,
+                solo=None, latency_variant=None) -> CacheConfig:
     return CacheConfig(batch, num_q_heads, num_kv_heads, head_dim, budget, DTYPES[out_dtype],
-                       float(softmax_scale), MODES[mode], KERNELS[kernel], split_tokens)
+                       float(softmax_scale), MODES[mode], KERNELS[kernel], split_tokens, plan_batch, seq_offset,
+                       ctas_per_sm, _SOLO[solo], _LAT[latency_variant])
 
 
 def cache_bytes(cfg: CacheConfig) -> int:
@@ -126,15 +134,18 @@ class Cache:
     """A static KV cache on one GPU plus the fused decode step (lf_decode_step).
 
     By default the slab is a torch uint8 CUDA tensor passed as caller-owned device memory
-    (`library_owned=True` makes the library do its single cudaMalloc instead).
+    (`library_owned=True` makes the library do its single cudaMalloc instead).  A rank's shard of a
+    global batch passes plan_batch (the global batch) and seq_offset (its first sequence) so every
+    unit is computed exactly as on one GPU; ctas_per_sm / solo / latency_variant override the plan.
     """
 
     def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32",
                  softmax_scale=0.0, kernel="auto", split_tokens=0, device=0, library_owned=False,
-                 mode="same_step"):
+                 mode="same_step", plan_batch=0, seq_offset=0, ctas_per_sm=0, solo=None, latency_variant=None):
         lib = load()
         self.cfg = make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype, softmax_scale,
-                               kernel, split_tokens, mode)
+                               kernel, split_tokens, mode, plan_batch, seq_offset, ctas_per_sm, solo,
+                               latency_variant)
         self.B, self.Hq, self.Hkv, self.d, self.N = batch, num_q_heads, num_kv_heads, head_dim, budget
         self.G = num_q_heads // num_kv_heads
         self.out_dtype = out_dtype
@@ -232,11 +243,12 @@ class Cache:
     def plan(self):
         k, s, c = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         _check(load().lf_cache_plan(self._h, ctypes.byref(k), ctypes.byref(s), ctypes.byref(c)), "plan")
-        cl, st, tc, sm, so = (ctypes.c_int32() for _ in range(5))
+        cl, st, tc, sm, so, lt = (ctypes.c_int32() for _ in range(6))
         _check(load().lf_cache_plan_detail(self._h, ctypes.byref(cl), ctypes.byref(st), ctypes.byref(tc),
-                                           ctypes.byref(sm), ctypes.byref(so)), "plan_detail")
+                                           ctypes.byref(sm), ctypes.byref(so), ctypes.byref(lt)), "plan_detail")
         return dict(kernel=KERNEL_NAMES[k.value], splits=s.value, split_tokens=c.value, clusters=cl.value,
-                    stages=st.value, tmem_cols=tc.value, smem=sm.value, solo_rounds=so.value)
+                    stages=st.value, tmem_cols=tc.value, smem=sm.value, solo_rounds=so.value,
+                    latency_variant=lt.value)
 
     def set_trace(self, buf):
         """Debug: device buffer for the -DLF_TRACE event trace (None disables)."""

@@ -64,7 +64,7 @@ struct Xchg {
 };
 
 struct TcSmem {
-    int ring, q, pbuf, L, xb, misc, ostage, kvn, red, bars, tmem, total;
+    int ring, q, pbuf, L, xb, misc, ostage, kvn, red, bars, tmem, nsm, total;
 };
 __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxNG) {
     TcSmem s;
@@ -80,6 +80,7 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxN
     s.red = off;  off += (2 * kNG * 4 * 16 + 2 * kNG * 4) * 4;
     s.bars = off; off += 48 * 8;
     s.tmem = off; off += 16;
+    s.nsm = off;  off += 8 * 4;                  // n_valid of the CTA's items, ring of 8 (NRDY)
     s.total = off + 1024;                        // slack for 1024-byte alignment of the base
     return s;
 }
@@ -90,7 +91,10 @@ constexpr int EMPTY = FULL + kMaxStages;
 constexpr int PREADY = EMPTY + kMaxStages, PFREE = PREADY + kMaxNG;
 constexpr int QFULL = PFREE + kMaxNG, QFREE = QFULL + 2, KDONE = QFREE + 2, SFREE = KDONE + 2;
 constexpr int OFULL = SFREE + 2, OFREE = OFULL + 1;
-constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2, NBARS = XFREE + 2;
+constexpr int XREADY = OFREE + 1, KREADY = XREADY + 2, XFREE = KREADY + 2;
+// NRDY[i % 8]: the producer published item i's fill state n (the ONLY read of n_valid in the CTA, so
+// every role agrees on the item's tile count even if a caller races a write to n_valid)
+constexpr int NRDY = XFREE + 2, NBARS = NRDY + 8;
 static_assert(NBARS <= 48, "barrier slots");
 
 // Debug event trace (-DLF_TRACE): %clock64 at fixed points, [cta][unit % 64][32] u64; slot 31 of
@@ -111,6 +115,13 @@ static_assert(NBARS <= 48, "barrier slots");
 #endif
 // per-tile events of the first units (debug): K tile t landed (MMA warp) in row ui+32, P of V tile t
 // ready in row ui+33 (t < 32)
+#ifdef LF_HANG_DIAG
+#define LF_PROG(role_, v_) ptx::hang_progress((role_), (unsigned long long)(v_))
+#else
+#define LF_PROG(role_, v_) \
+    do {                   \
+    } while (0)
+#endif
 #define LF_TILE_EVENT(ui_, row_, t_)            \
     do {                                        \
         if ((t_) < 32) LF_EVENT((ui_) + (row_), (t_)); \
@@ -127,19 +138,27 @@ struct UnitInfo {
     int u, b, h, n, c0, c1, nv, ntiles;
     bool split, valid;
 };
-// Work item i of CTA s of cluster cid (all roles walk the same list).  `solo_rounds` rounds of
-// whole units, one per CTA with no exchange (P = C*S units per round), then the remaining units
-// split S ways across the cluster: balanced tails without paying the exchange on every unit.
-__device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int s, int C, int i) {
+// Number of whole ("solo") units CTA j = cid*S + s of a grid of P = C*S CTAs computes: units
+// j, j + P, j + 2P, ... below solo_units.
+__device__ __forceinline__ int solo_items(const StepParams& p, int cid, int s, int C) {
+    const int P = C * p.splits, j = cid * p.splits + s;
+    return p.solo_units > j ? (p.solo_units - j + P - 1) / P : 0;
+}
+// Work item i of CTA s of cluster cid (all roles walk the same list): first its whole units, one
+// per CTA with no exchange, then the units from solo_units on, split S ways across the cluster
+// (cluster cid takes solo_units + cid, + C, ...): balanced tails without paying the exchange on
+// every unit.  Which units are whole is part of the plan of the plan_batch problem (lf_runtime.cu),
+// so a shard computes every unit exactly as the one-GPU cache does.
+__device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int s, int C, int i, int R) {
     UnitInfo x;
     const int S = p.splits, P = C * S;
     bool split;
     int u;
-    if (i < p.solo_rounds) {
-        u = i * P + cid * S + s;
+    if (i < R) {
+        u = cid * S + s + i * P;
         split = false;
     } else {
-        u = p.solo_rounds * P + cid + (i - p.solo_rounds) * C;
+        u = p.solo_units + cid + (i - R) * C;
         split = S > 1;
     }
     x.valid = u < p.B * p.Hkv;
@@ -152,19 +171,16 @@ __device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int 
     x.c1 = split ? min(x.c0 + p.chunk, p.N) : p.N;
     return x;
 }
-// ... plus the unit's fill state (read after the PDL wait: the previous step may have appended)
-__device__ __forceinline__ UnitInfo item_info(const StepParams& p, int cid, int s, int C, int i) {
-    UnitInfo x = item_base(p, cid, s, C, i);
-    if (!x.valid) return x;
-    x.n = __ldcg(p.n_valid + x.u);
+// ... plus the unit's fill state n (after the PDL wait: the previous step may have appended)
+__device__ __forceinline__ void set_fill(UnitInfo& x, int n) {
+    x.n = n;
     x.nv = max(0, min(x.c1, x.n) - x.c0);
     x.ntiles = (x.nv + 127) / 128;
-    return x;
 }
 // tokens one CTA may hold for a unit (TMEM regions, lambda buffer)
-__host__ __device__ inline int tc_hold(int N, int chunk, int solo_rounds) {
+__host__ __device__ inline int hold_tokens(int N, int chunk, bool solo) {
     const int Nr = (N + 127) / 128 * 128;
-    return solo_rounds > 0 && Nr > chunk ? Nr : chunk;
+    return solo && Nr > chunk ? Nr : chunk;
 }
 
 // kLat: the latency variant for split plans whose grid leaves SMs free (small batches, where the
@@ -179,8 +195,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     const StepParams& p = a.p;
     // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const int G = p.G, N = p.N, chunk = p.chunk, ST = a.stages;
-    const int hold = tc_hold(N, chunk, p.solo_rounds);
+    const int G = p.G, N = p.N, ST = a.stages;
+    const int hold = p.hold;
     const TcSmem so = tc_smem(hold, ST, kNG);
     float* Ls = (float*)(smem + so.L);
     Xchg* xb = (Xchg*)(smem + so.xb);
@@ -202,6 +218,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     const int s = (int)cluster.block_rank();
     const int cid = blockIdx.x / S;
     const int C = a.clusters;
+    const int R = solo_items(p, cid, s, C);   // whole units of this CTA (its first R items)
+    volatile int* nsm = (volatile int*)(smem + so.nsm);
 
     if (tid == 0) {
         for (int i = 0; i < ST; ++i) {
@@ -221,12 +239,19 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::mbar_init(BAR(KREADY + i), 1);
             ptx::mbar_init(BAR(XFREE + i), S);
         }
+        for (int i = 0; i < 8; ++i) ptx::mbar_init(BAR(NRDY + i), 1);
         ptx::mbar_init(BAR(OFULL), 1);
         ptx::mbar_init(BAR(OFREE), 4);
         ptx::fence_mbar_init();
         ptx::tma_prefetch_desc(&a.tmK);
         ptx::tma_prefetch_desc(&a.tmV);
     }
+#ifdef LF_HANG_DIAG
+    if (tid == 0) {
+        ptx::g_hang_log = p.trace;
+        ptx::hang_progress(8, bars);
+    }
+#endif
     if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(smem + so.tmem), (uint32_t)a.tmem_cols);
     if (tid == 0) LF_EVENT(0, 16);
 #ifdef LF_TRACE
@@ -237,7 +262,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     }
 #endif
     if (tid == 64) {   // L2 warm-up of the first item's operands; safe before the PDL wait (L2 is coherent)
-        const UnitInfo x = item_base(p, cid, s, C, 0);
+        const UnitInfo x = item_base(p, cid, s, C, 0, R);
         if (x.valid) {
             const int u = x.u;
             ptx::bulk_prefetch_l2(p.n_valid + (u & ~3), 16);
@@ -274,17 +299,20 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             for (int i = 0;; ++i, ++qi) {
                 // every global read of the item goes out at once (Q rows, fill state):
                 // one L2 round trip instead of a chain of them before the first MMA
-                UnitInfo x = item_base(p, cid, s, C, i);
+                UnitInfo x = item_base(p, cid, s, C, i, R);
                 if (!x.valid) break;
+                if (lane == 0) LF_PROG(0, ((unsigned long long)i << 32) | it);
                 const int u = x.u;
                 const int qb = qi & 1;
                 const uint4* qg = (const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128);
                 uint4 qv[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) qv[k] = lane + 32 * k < G * 16 ? __ldg(qg + lane + 32 * k) : make_uint4(0, 0, 0, 0);
-                x.n = __ldcg(p.n_valid + u);
-                x.nv = max(0, min(x.c1, x.n) - x.c0);
-                x.ntiles = (x.nv + 127) / 128;
+                set_fill(x, __ldcg(p.n_valid + u));
+                if (lane == 0) {   // publish n: the only read of n_valid in the CTA
+                    nsm[i & 7] = x.n;
+                    ptx::mbar_arrive(BAR(NRDY + (i & 7)));
+                }
                 if (lane == 0 && i == 0) LF_EVENT(0, 22);
                 // the first ring stages go out before Q is staged (they do not depend on it)
                 const int pre = min(2 * x.ntiles, ST);
@@ -323,8 +351,14 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         } else {
             uint32_t it = 0, qi = 0;
             for (int i = 0;; ++i, ++qi) {
-                const UnitInfo x = item_info(p, cid, s, C, i);
+                UnitInfo x = item_base(p, cid, s, C, i, R);
                 if (!x.valid) break;
+                if (lane == 0) LF_PROG(0, ((unsigned long long)i << 32) | it);
+                set_fill(x, __ldcg(p.n_valid + x.u));
+                if (lane == 0) {   // publish n: the only read of n_valid in the CTA
+                    nsm[i & 7] = x.n;
+                    ptx::mbar_arrive(BAR(NRDY + (i & 7)));
+                }
                 const int u = x.u;
                 const int qb = qi & 1;
                 // the first ring stages go out before Q is staged (they do not depend on it)
@@ -366,11 +400,17 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         if (lane == 0) {
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
-            uint32_t it = 0, pi = 0, ui = 0;
+            uint32_t it = 0, ui = 0;
+            uint32_t pc[kNG];   // V tiles handed to each softmax group so far (PREADY / PFREE phases)
+#pragma unroll
+            for (int g = 0; g < kNG; ++g) pc[g] = 0;
             for (int i = 0;; ++i, ++ui) {
-                const UnitInfo x = item_info(p, cid, s, C, i);
+                UnitInfo x = item_base(p, cid, s, C, i, R);
                 if (!x.valid) break;
+                ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
+                set_fill(x, nsm[i & 7]);
                 const uint32_t par = ui & 1u;
+                LF_PROG(1, ((unsigned long long)i << 32) | it);
                 ptx::mbar_wait(BAR(QFULL + par), (ui >> 1) & 1u);
                 ptx::mbar_wait(BAR(SFREE + par), ((ui >> 1) & 1u) ^ 1u);   // unit ui-2 finalised
                 ptx::mbar_wait(BAR(OFREE), (ui & 1u) ^ 1u);                  // O(ui-1) drained
@@ -395,11 +435,18 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::mma_commit(BAR(QFREE + par));
                 ptx::mma_commit(BAR(KDONE + par));
                 const uint32_t oreg = tmem + (par ^ 1u) * RC;
-                for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
+                for (int t = 0; t < x.ntiles; ++t, ++it) {                 // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    const int pb = pi % kNG;
-                    ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
+                    // tile t of a unit always goes to softmax group t % kNG, so each group's partial
+                    // Z sums a fixed set of the unit's tiles: the unit's arithmetic does not depend on
+                    // which units the CTA computed before it (shard invariance)
+                    const int pb = t % kNG;
+                    uint32_t k = 0;
+#pragma unroll
+                    for (int g = 0; g < kNG; ++g)
+                        if (g == pb) k = pc[g]++;
+                    ptx::mbar_wait(BAR(PREADY + pb), k & 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
@@ -469,13 +516,13 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             return best;
         };
-        uint32_t it = 0, pi = 0, ui = 0, xi = 0;
+        uint32_t it = 0, gc = 0, ui = 0, xi = 0;   // gc: V tiles this softmax group handled so far
         for (int i = 0;; ++i, ++ui) {
             UnitInfo x;
             uint4* kvn = (uint4*)(smem + so.kvn);
             if constexpr (kLat) {
                 // all global reads of the item at once: fill state, k*/v* rows, the x* operands
-                x = item_base(p, cid, s, C, i);
+                x = item_base(p, cid, s, C, i, R);
                 if (sidx == 0 && i == 0) LF_EVENT(0, 20);
                 if (!x.valid) break;
                 const int u = x.u;
@@ -490,9 +537,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     xq = __ldg((const uint4*)(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G + xg) * 128) + xch);
                     xk = __ldg((const uint4*)(p.k_new + (size_t)u * 128) + xch);
                 }
-                x.n = __ldcg(p.n_valid + u);
-                x.nv = max(0, min(x.c1, x.n) - x.c0);
-                x.ntiles = (x.nv + 127) / 128;
+                ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
+                set_fill(x, nsm[i & 7]);
                 if (sidx == 0 && i == 0) LF_EVENT(0, 21);
                 if (warp == 2 + 4 * kNG - 1) kvn[lane] = kvw;
                 if (sidx < 128) {
@@ -508,7 +554,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     if (xch == 0 && xg < G) xs[xg] = p.deferred ? -INFINITY : acc * sl2;
                 }
             } else {
-                x = item_info(p, cid, s, C, i);
+                x = item_base(p, cid, s, C, i, R);
                 if (!x.valid) break;
                 const int u = x.u;
                 // stage the current token's k*, v* rows (combine + eviction write read them later)
@@ -528,6 +574,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
                     if (lane == 0) xs[g] = p.deferred ? -INFINITY : acc * sl2;
                 }
+                ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
+                set_fill(x, nsm[i & 7]);
             }
             const int u = x.u;
             const int nv = x.nv;
@@ -538,7 +586,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             // latency variant, one tile per CTA: its V tile lands with (or before) K, so lambda_j and
             // the zeroing of rows past n happen while the QK MMA runs (PREADY still follows them)
             const bool lam_first = kLat && x.ntiles == 1;
-            if (lam_first && (int)(pi % kNG) == grp) {
+            if (lam_first && grp == 0) {
                 const uint32_t iv = it + 1;
                 const int st = iv % ST;
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);
@@ -598,13 +646,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             float z[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) z[g] = 0.f;
-            for (int t = 0; t < x.ntiles; ++t) {
-                const uint32_t c = pi + t;
-                if ((int)(c % kNG) != grp) continue;
-                const int pb = c % kNG;
+            for (int t = grp; t < x.ntiles; t += kNG, ++gc) {   // tile t -> group t % kNG (fixed per unit)
+                const int pb = grp;
                 uint32_t r[8];
                 ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNG) & 1u) ^ 1u);
+                ptx::mbar_wait(BAR(PFREE + pb), (gc & 1u) ^ 1u);
                 ptx::tmem_ld_wait();
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
@@ -649,7 +695,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
                 if (lane == 0 && q4 == 0) LF_TILE_EVENT(ui, 33, t);
             }
-            pi += x.ntiles;
             it += 2 * x.ntiles;
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
@@ -1038,14 +1083,6 @@ int max_active_clusters(int splits, int smem) {
         cudaGetLastError();
         return 0;
     }
-    if (getenv("LF_DEBUG_PLAN")) {
-        int b = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tc_decode_kernel<GP, NG, kLat>, 64 + 128 * NG, smem);
-        cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, tc_decode_kernel<GP, NG, kLat>);
-        fprintf(stderr, "[lf plan] NG=%d smem=%d blocks/SM=%d regs=%d maxdyn=%d clusters=%d\n", NG, smem, b,
-                fa.numRegs, fa.maxDynamicSharedSizeBytes, n);
-    }
     return n;
 }
 
@@ -1113,7 +1150,7 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 1 && G <= 8; }
 // with the measured unit-boundary overheads in streamed tokens (ovh_1 ~ 128 alone, ovh_S ~ 1024
 // with the cross-CTA exchange).  Solo rounds process whole units per CTA (no exchange); the
 // remaining units are split S ways, which balances the tail.
-Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
+Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, const PlanForce& force) {
     (void)d;
     Plan best;
     best.lat = 0;
@@ -1133,8 +1170,10 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
         if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
         if (splits > 16 || chunk > kMaxChunk) continue;
         for (int k = 1; k <= 2; ++k) {
+            if (force.ctas_per_sm && k != force.ctas_per_sm) continue;
             for (int solo = 0; solo <= 1; ++solo) {
-                if (solo && (splits == 1 || Nr > kMaxChunk || split_tokens > 0)) continue;
+                if (force.solo && solo != force.solo - 1) continue;
+                if (solo && (splits == 1 || Nr > kMaxChunk)) continue;
                 const int hold = solo ? max(Nr, chunk) : chunk;
                 const int tiles = (hold + 127) / 128;
                 const int ng = k == 1 ? kMaxNG : 1;
@@ -1159,13 +1198,8 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                 // fit (2 x 93 KB SMEM, 2 x 30K registers, 2 x 256 TMEM columns); measured on B200 the
                 // two co-reside (e.g. 512 x N=512: 200 -> 166 us), so the k = 2 grid is doubled.  The
                 // persistent loop is correct either way (no cross-cluster dependency).
-                static const bool no_double = getenv("LF_NO_K2_DOUBLE") != nullptr;   // stall probe (DESIGN 14)
-                if (k == 2 && !no_double) C *= 2;
+                if (k == 2) C *= 2;
                 if (C <= 0) continue;
-                if (const char* f = getenv("LF_FORCE_PLAN")) {   // debug: "S,k,solo"
-                    int fs = 0, fk = 0, fo = -1;
-                    if (sscanf(f, "%d,%d,%d", &fs, &fk, &fo) == 3 && (fs != splits || fk != k || fo != solo)) continue;
-                }
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
                 long long cost, R = 0;
                 int Cu;
@@ -1179,9 +1213,6 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
                     Cu = C < units ? C : units;
                     cost = ((units + Cu - 1) / Cu) * ((long long)k * chunk + ovhS / k);
                 }
-                if (getenv("LF_DEBUG_PLAN"))
-                    fprintf(stderr, "[lf plan] S=%d chunk=%d k=%d solo=%d stages=%d smem=%d C=%d R=%lld cost=%lld\n",
-                            splits, chunk, k, solo, st, smem, C, R, cost);
                 if (best_cost < 0 || cost < best_cost) {
                     best_cost = cost;
                     best.splits = splits;
@@ -1199,9 +1230,12 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms) {
     // latency variant: split plans whose grid leaves SMs free (measured: it helps the split
     // exchange chain of small batches; solo and machine-filling plans stay on the streaming code)
     if (best.splits > 1)
-        best.lat = (long long)best.clusters * best.splits < (long long)num_sms * (best.tmem_cols == 256 ? 2 : 1);
+        best.lat = force.lat ? force.lat - 1
+                             : (long long)best.clusters * best.splits < (long long)num_sms * (best.tmem_cols == 256 ? 2 : 1);
     return best;
 }
+
+int tc_hold(const Plan& plan, int N) { return hold_tokens(N, plan.chunk, plan.solo_rounds > 0); }
 
 bool tc_make_maps(TcMaps* maps, void* K, void* V, long long units, int N, int d) {
     static_assert(sizeof(CUtensorMap) <= sizeof(maps->k), "tensor map size");

@@ -28,13 +28,22 @@ struct StepParams {
     float scale_log2;       // softmax_scale * log2(e): logits live in log2 units on chip
     int32_t splits;         // CTAs per unit (= cluster size)
     int32_t chunk;          // tokens per CTA (multiple of 128)
-    int32_t solo_rounds;    // tcgen05 kernel: rounds of whole units per CTA before the split tail
+    int32_t solo_units;     // tcgen05 kernel: units [0, solo_units) are computed whole by one CTA each
+                            // (round-robin over the grid's CTAs); the rest split across their cluster
+    int32_t hold;           // tcgen05 kernel: tokens one CTA holds for a unit (TMEM regions, lambda buffer)
 };
 
 // launch attributes shared by the decode kernels: cluster dims + programmatic dependent launch
 // (the kernels call griddepcontrol.wait before their first dependent global access); LF_NO_PDL=1
 // disables the latter
 int fill_launch_attrs(cudaLaunchAttribute* attr, int cluster_x);
+
+// Plan overrides (lf_cache_config ctas_per_sm / solo / latency_variant; 0 = automatic)
+struct PlanForce {
+    int32_t ctas_per_sm;
+    int32_t solo;
+    int32_t lat;
+};
 
 struct Plan {
     int32_t kernel;   // lf_kernel (resolved: SIMT or TCGEN05)
@@ -74,7 +83,8 @@ struct TcMaps {               // two CUtensorMap (K, V) encoded once per cache (
     alignas(64) unsigned char v[128];
 };
 bool tc_supported(int G, int d);
-Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms);
+Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, const PlanForce& force);
+int tc_hold(const Plan& plan, int N);
 bool tc_make_maps(TcMaps* maps, void* K, void* V, long long units, int N, int d);
 cudaError_t tc_launch(const StepParams& p, const Plan& plan, const TcMaps& maps, cudaStream_t stream);
 

@@ -81,7 +81,17 @@ lf_status validate(const lf_cache_config* c) {
         return fail(LF_ERR_UNSUPPORTED, "head_dim %d not built (64, 128)", c->head_dim);
     int G = c->num_q_heads / c->num_kv_heads;
     if (G > 16) return fail(LF_ERR_UNSUPPORTED, "group size %d > 16 not built", G);
-    if ((long long)c->batch * c->num_kv_heads > 0x7fffffff / 2)
+    if (c->plan_batch < 0 || c->seq_offset < 0)
+        return fail(LF_ERR_INVALID_ARGUMENT, "plan_batch and seq_offset must be >= 0");
+    if (c->plan_batch == 0 && c->seq_offset != 0)
+        return fail(LF_ERR_INVALID_ARGUMENT, "seq_offset %d needs plan_batch (the global batch)", c->seq_offset);
+    if (c->plan_batch > 0 && (long long)c->seq_offset + c->batch > c->plan_batch)
+        return fail(LF_ERR_INVALID_ARGUMENT, "sequences [%d, %d) exceed plan_batch %d", c->seq_offset,
+                    c->seq_offset + c->batch, c->plan_batch);
+    if (c->ctas_per_sm < 0 || c->ctas_per_sm > 2 || c->solo < 0 || c->solo > 2 || c->latency_variant < 0 ||
+        c->latency_variant > 2)
+        return fail(LF_ERR_INVALID_ARGUMENT, "plan overrides must be 0 (automatic), 1 or 2");
+    if ((long long)(c->plan_batch > c->batch ? c->plan_batch : c->batch) * c->num_kv_heads > 0x7fffffff / 2)
         return fail(LF_ERR_INVALID_ARGUMENT, "too many units");
     if (c->budget > 65536) return fail(LF_ERR_UNSUPPORTED, "budget %d > 65536 not built", c->budget);
     return LF_OK;
@@ -94,8 +104,9 @@ __global__ void fill_i32(int32_t* p, int32_t v, int n) {
 
 // Deferred mode pre-pass (Fig. 2 left): one warp per unit.  The current token covers the
 // slot chosen at the previous step when the unit is full, else it is appended at n (R11);
-// slot[u] returns where it went.  A full unit without a pending slot (cannot happen through the
-// API: every step of a full unit sets one) falls back to slot 0.
+// slot[u] returns where it went.  A full unit always has a pending slot here: every step sets one
+// and lf_decode_step refuses a sequence whose prefill filled the whole budget (R26); the
+// fallback to slot 0 only guards against a caller overwriting pend through the views.
 __global__ void deferred_write_kernel(lf::StepParams p) {
     const int u = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -124,7 +135,10 @@ struct lf_cache {
     size_t slab_bytes;
     bool owns;
     Layout L;
-    lf::Plan plan;
+    lf::Plan plan;       // the plan of the plan_batch problem (fixes every unit's reduction order)
+    int32_t launch_clusters;   // clusters launched for THIS cache's units
+    int32_t solo_units;        // this cache's units [0, solo_units) are computed whole by one CTA
+    std::vector<unsigned char> needs_pend;   // deferred modes: sequence full after prefill, no victim yet
     lf::TcMaps maps;
     unsigned long long* trace;
     char* host_stage;      // pinned staging for small lf_decode_step_host calls (one H2D + one D2H)
@@ -144,12 +158,10 @@ size_t stage_out_bytes(const Layout& L, const lf_cache_config& g) {
 
 namespace lf {
 int fill_launch_attrs(cudaLaunchAttribute* attr, int cluster_x) {
-    static const bool no_pdl = getenv("LF_NO_PDL") != nullptr;
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cluster_x;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    if (no_pdl) return 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     return 2;
@@ -167,46 +179,62 @@ namespace {
 lf_status make_plan(lf_cache* c) {
     const lf_cache_config& g = c->cfg;
     int G = g.num_q_heads / g.num_kv_heads;
-    int units = g.batch * g.num_kv_heads;
+    const int units = g.batch * g.num_kv_heads;
+    const int plan_units = (g.plan_batch > 0 ? g.plan_batch : g.batch) * g.num_kv_heads;
     bool want_tc = g.kernel == LF_KERNEL_TCGEN05 ||
                    (g.kernel == LF_KERNEL_AUTO && lf::tc_supported(G, g.head_dim));
+    c->solo_units = 0;
     if (want_tc) {
         if (!lf::tc_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "tcgen05 kernel not built for G=%d d=%d", G, g.head_dim);
-        // The plan depends only on the shape and the device (occupancy queries: ~1 ms per plan), and
-        // a model creates one cache per layer with the same shape: memoise it per process.
+        // The plan depends only on the problem shape, the overrides and the device (occupancy queries:
+        // ~1 ms per plan), and a model creates one cache per layer with the same shape: memoise it.
         struct Key {
-            int dev, units, G, d, N, split, sms;
+            int dev, units, G, d, N, split, sms, k, solo, lat;
             bool operator==(const Key& o) const {
                 return dev == o.dev && units == o.units && G == o.G && d == o.d && N == o.N && split == o.split &&
-                       sms == o.sms;
+                       sms == o.sms && k == o.k && solo == o.solo && lat == o.lat;
             }
         };
         static std::mutex mu;
         static std::vector<std::pair<Key, lf::Plan>> memo;
-        const Key k{c->device, units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms};
-        const bool forced = getenv("LF_FORCE_PLAN") != nullptr || getenv("LF_DEBUG_PLAN") != nullptr;
+        const Key k{c->device, plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms,
+                    g.ctas_per_sm, g.solo, g.latency_variant};
         bool hit = false;
         {
             std::lock_guard<std::mutex> lock(mu);
             for (const auto& e : memo)
-                if (!forced && e.first == k) {
+                if (e.first == k) {
                     c->plan = e.second;
                     hit = true;
                     break;
                 }
         }
         if (!hit) {
-            c->plan = lf::tc_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
-            if (!forced && c->plan.splits > 0) {
+            const lf::PlanForce force{g.ctas_per_sm, g.solo, g.latency_variant};
+            c->plan = lf::tc_plan(plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms, force);
+            if (c->plan.splits > 0) {
                 std::lock_guard<std::mutex> lock(mu);
                 memo.push_back({k, c->plan});
             }
         }
+        if (c->plan.splits < 1)
+            return fail(LF_ERR_UNSUPPORTED, "no tcgen05 plan for budget %d, split_tokens %d and the overrides "
+                        "(ctas_per_sm %d, solo %d, latency_variant %d)", g.budget, g.split_tokens,
+                        g.ctas_per_sm, g.solo, g.latency_variant);
+        // this cache's share of the plan_batch problem: the same units are whole or split as there
+        const long long P = (long long)c->plan.clusters * c->plan.splits;
+        long long gsolo = (long long)c->plan.solo_rounds * P;
+        if (gsolo > plan_units) gsolo = plan_units;
+        long long ls = gsolo - (long long)g.seq_offset * g.num_kv_heads;
+        c->solo_units = (int32_t)(ls < 0 ? 0 : ls > units ? units : ls);
+        c->launch_clusters = c->plan.clusters;
+        if (c->solo_units == 0 && c->launch_clusters > units) c->launch_clusters = units;
     } else {
         if (!lf::simt_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "CUDA-core kernel not built for G=%d d=%d", G, g.head_dim);
-        c->plan = lf::simt_plan(units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+        c->plan = lf::simt_plan(plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+        c->launch_clusters = 0;
     }
     if (c->plan.splits < 1 || c->plan.splits > 16)
         return fail(LF_ERR_UNSUPPORTED, "split plan out of range (%d splits)", c->plan.splits);
@@ -266,6 +294,7 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     c->L = layout_of(c->cfg);
+    c->needs_pend.assign((size_t)cfg->batch, 0);
     if ((s = make_plan(c)) != LF_OK) { delete c; cudaSetDevice(prev); return s; }
     if (device_buf) {
         if (buf_bytes < c->L.total || ((uintptr_t)device_buf & 255)) {
@@ -349,10 +378,11 @@ lf_status lf_cache_plan(const lf_cache* c, int32_t* kernel, int32_t* splits, int
 }
 
 lf_status lf_cache_plan_detail(const lf_cache* c, int32_t* clusters, int32_t* stages, int32_t* tmem_cols,
-                                int32_t* smem_bytes, int32_t* solo_rounds) {
+                                int32_t* smem_bytes, int32_t* solo_rounds, int32_t* latency_variant) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
     if (solo_rounds) *solo_rounds = c->plan.solo_rounds;
-    if (clusters) *clusters = c->plan.clusters;
+    if (latency_variant) *latency_variant = c->plan.lat;
+    if (clusters) *clusters = c->launch_clusters;
     if (stages) *stages = c->plan.stages;
     if (tmem_cols) *tmem_cols = c->plan.tmem_cols;
     if (smem_bytes) *smem_bytes = c->plan.smem;
@@ -371,6 +401,21 @@ lf_status lf_debug_set_trace(lf_cache* c, void* device_buf) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
     c->trace = (unsigned long long*)device_buf;
     return LF_OK;
+}
+
+// After a prefill of n tokens: n_valid = n for every kv head of `seq`, no pending victim (deferred
+// modes), and a sequence whose prefill filled the whole budget is marked: its first deferred step
+// would have no slot to cover (R26)
+static cudaError_t reset_seq(lf_cache* c, int32_t seq, int32_t n, cudaStream_t st) {
+    const lf_cache_config& g = c->cfg;
+    char* base = (char*)c->slab;
+    const int blocks = (g.num_kv_heads + 255) / 256;
+    int32_t* nv = (int32_t*)(base + c->L.nv_off) + (size_t)seq * g.num_kv_heads;
+    int32_t* pd = (int32_t*)(base + c->L.pd_off) + (size_t)seq * g.num_kv_heads;
+    fill_i32<<<blocks, 256, 0, st>>>(nv, n, g.num_kv_heads);
+    fill_i32<<<blocks, 256, 0, st>>>(pd, -1, g.num_kv_heads);
+    if (g.mode != LF_EVICT_SAME_STEP) c->needs_pend[seq] = n >= g.budget;
+    return cudaGetLastError();
 }
 
 lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v, int32_t n,
@@ -398,11 +443,7 @@ lf_status lf_prefill_fill(lf_cache* c, int32_t seq, const void* k, const void* v
         if (e == cudaSuccess)
             e = cudaMemcpy2DAsync(V, unit, v, n * row, n * row, g.num_kv_heads, cudaMemcpyDeviceToDevice, st);
     }
-    if (e == cudaSuccess) {
-        int32_t* nv = (int32_t*)(base + c->L.nv_off) + (size_t)seq * g.num_kv_heads;
-        fill_i32<<<1, 256, 0, st>>>(nv, n, g.num_kv_heads);
-        e = cudaGetLastError();
-    }
+    if (e == cudaSuccess) e = reset_seq(c, seq, n, st);
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "prefill");
     return LF_OK;
@@ -443,10 +484,13 @@ lf_status lf_prefill_snapkv(lf_cache* c, int32_t seq, const void* k, const void*
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     char* base = (char*)c->slab;
-    cudaError_t e = lf::snapkv_launch((uint16_t*)(base + c->L.k_off), (uint16_t*)(base + c->L.v_off),
-                                      (int32_t*)(base + c->L.nv_off), seq, g.num_kv_heads,
-                                      g.num_q_heads / g.num_kv_heads, g.head_dim, g.budget, k, v, q_obs, n, w,
-                                      pool_kernel, g.softmax_scale, kept, workspace, (cudaStream_t)stream);
+    cudaError_t e = reset_seq(c, seq, 0, (cudaStream_t)stream);
+    if (e == cudaSuccess)
+        e = lf::snapkv_launch((uint16_t*)(base + c->L.k_off), (uint16_t*)(base + c->L.v_off),
+                              (int32_t*)(base + c->L.nv_off), seq, g.num_kv_heads, g.num_q_heads / g.num_kv_heads,
+                              g.head_dim, g.budget, k, v, q_obs, n, w, pool_kernel, g.softmax_scale, kept,
+                              workspace, (cudaStream_t)stream);
+    if (g.mode != LF_EVICT_SAME_STEP) c->needs_pend[seq] = 1;   // SnapKV fills the whole budget
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "snapkv");
     return LF_OK;
@@ -495,7 +539,19 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
     if (!q || !k_new || !v_new || !out || !slot)
         return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new, out and slot must be non-NULL");
+    // the kernels move q, k_new, v_new and out in 16-byte vectors
+    if (((uintptr_t)q | (uintptr_t)k_new | (uintptr_t)v_new | (uintptr_t)out) & 15)
+        return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new and out must be 16-byte aligned");
+    if (((uintptr_t)slot | (uintptr_t)scores) & 3)
+        return fail(LF_ERR_INVALID_ARGUMENT, "slot and scores must be 4-byte aligned");
     const lf_cache_config& g = c->cfg;
+    if (g.mode != LF_EVICT_SAME_STEP)
+        for (int b = 0; b < g.batch; ++b)
+            if (c->needs_pend[b])
+                return fail(LF_ERR_INVALID_ARGUMENT,
+                            "deferred mode: sequence %d was prefilled to the whole budget, so there is no slot "
+                            "chosen at a previous step for its current token to cover (Fig. 2, P:152; R26); "
+                            "prefill fewer than budget tokens or use LF_EVICT_SAME_STEP", b);
     char* base = (char*)c->slab;
     lf::StepParams p;
     p.q = (const uint16_t*)q;
@@ -522,15 +578,18 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.scale_log2 = (float)((double)g.softmax_scale * 1.4426950408889634);
     p.splits = c->plan.splits;
     p.chunk = c->plan.chunk;
-    p.solo_rounds = c->plan.solo_rounds;
+    p.solo_units = c->solo_units;
+    p.hold = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_hold(c->plan, g.budget) : 0;
+    lf::Plan lp = c->plan;
+    lp.clusters = c->launch_clusters;
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);
     cudaError_t e = cudaSuccess;
     if (p.deferred) e = lf::deferred_write_launch(p, (cudaStream_t)stream);
     if (e == cudaSuccess)
-        e = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_launch(p, c->plan, c->maps, (cudaStream_t)stream)
-                                                 : lf::simt_launch(p, c->plan, (cudaStream_t)stream);
+        e = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_launch(p, lp, c->maps, (cudaStream_t)stream)
+                                                 : lf::simt_launch(p, lp, (cudaStream_t)stream);
     if (prev != c->device) cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "decode launch");
     return LF_OK;

@@ -32,6 +32,67 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+#ifdef LF_HANG_DIAG
+// Protocol debugging (-DLF_HANG_DIAG, never the product build): a wait that has not completed after
+// ~1 s records (barrier address, parity, raw barrier word, time) into the per-thread row of a log in
+// mapped host memory (the cache's debug buffer, lf_debug_set_trace) and keeps waiting, so the host can
+// read which barriers every stuck thread waits on while the kernel hangs (tools/hang_diag.py).
+// Row layout: 8 u64 per thread, [blockIdx.x * blockDim.x + threadIdx.x]; rows 0.. of the CTA region.
+static __device__ unsigned long long* volatile g_hang_log;
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+static __device__ __noinline__ void hang_note(uint32_t bar, uint32_t parity, uint32_t kind) {
+    unsigned long long* L = g_hang_log;
+    if (!L) return;
+    unsigned long long raw;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(raw) : "r"(bar) : "memory");
+    volatile unsigned long long* r = L + 8ull * ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x);
+    r[1] = ((unsigned long long)bar << 32) | ((unsigned long long)kind << 8) | parity;
+    r[2] = raw;
+    r[3] = gtimer();
+    __threadfence_system();
+    r[0] = 0x4c46484e47ull;   // "LFHNG": row valid
+    __threadfence_system();
+}
+// progress counters of a role: row [grid threads + blockIdx.x * 16 + role] (role 8: barrier base)
+__device__ __forceinline__ void hang_progress(int role, unsigned long long v) {
+    unsigned long long* L = g_hang_log;
+    if (!L) return;
+    volatile unsigned long long* r = L + 8ull * gridDim.x * blockDim.x + 16ull * blockIdx.x + role;
+    *r = v;
+}
+#define LF_DIAG_WAIT(TRY, bar, parity, kind)                                   \
+    do {                                                                       \
+        unsigned long long t0_ = 0;                                            \
+        uint32_t n_ = 0;                                                       \
+        bool noted_ = false;                                                   \
+        while (!(TRY)) {                                                       \
+            if ((++n_ & 255u) == 0 && !noted_) {                              \
+                const unsigned long long t_ = gtimer();                        \
+                if (t0_ == 0) t0_ = t_;                                        \
+                else if (t_ - t0_ > 1000000000ull) {                           \
+                    hang_note(bar, parity, kind);                              \
+                    noted_ = true;                                             \
+                }                                                              \
+            }                                                                  \
+        }                                                                      \
+    } while (0)
+__device__ __forceinline__ bool mbar_try_wait_cluster(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+#endif
+
 // Waits.  The product build spins in ONE asm loop {try_wait; @!p bra} -- measured on B200
 // (tools/probes/tma_probe2.cu, 32 KB TMA ring, one SM): this exact loop lets TMA fill the ring at
 // 259 cycles per stage, while any extra instruction in the loop (an iteration bound, a clock read,
@@ -39,7 +100,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 // -DLF_BOUNDED_WAITS (debug / protocol-development builds) traps after ~2^28 retries instead of
 // hanging the GPU on a protocol bug.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-#ifdef LF_BOUNDED_WAITS
+#if defined(LF_HANG_DIAG)
+    LF_DIAG_WAIT(mbar_try_wait(bar, parity), bar, parity, 1);
+#elif defined(LF_BOUNDED_WAITS)
     asm volatile(
         "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
         "LF_WAIT:\n\t"
@@ -71,7 +134,9 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_bar) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {   // acquire.cluster
-#ifdef LF_BOUNDED_WAITS
+#if defined(LF_HANG_DIAG)
+    LF_DIAG_WAIT(mbar_try_wait_cluster(bar, parity), bar, parity, 2);
+#elif defined(LF_BOUNDED_WAITS)
     asm volatile(
         "{\n\t.reg .pred p;\n\t.reg .u32 n;\n\tmov.u32 n, 0;\n"
         "LF_WAIT:\n\t"

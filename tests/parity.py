@@ -124,11 +124,13 @@ def assert_cache_equal(cache, orc: oracle.OracleCache):
 
 
 def setup_pair(wl: Workload, kernel="auto", out_dtype="f32", seed=0, prefill=None, split_tokens=0,
-               sigma_s=2.0, scale=0.0, nthreads=4, key_outliers=False):
+               sigma_s=2.0, scale=0.0, nthreads=4, key_outliers=False, **plan_kw):
+    """(cache, oracle, synth) on the same seeded inputs; plan_kw: ctas_per_sm / solo /
+    latency_variant overrides of the split plan."""
     from paper_2603_11504_b200 import Cache
     syn = Synth(wl, seed=seed, sigma_s=sigma_s, key_outliers=key_outliers)
     cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, kernel=kernel,
-                  split_tokens=split_tokens, softmax_scale=scale)
+                  split_tokens=split_tokens, softmax_scale=scale, **plan_kw)
     orc = oracle.OracleCache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, scale=scale or None, nthreads=nthreads)
     n = wl.prefill if prefill is None else prefill
     if n > 0:

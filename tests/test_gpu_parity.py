@@ -78,6 +78,19 @@ def test_random_shapes(cuda_lib, kernel, shape):
 
 
 @pytest.mark.parametrize("kernel", KERNELS)
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "B{}_Hq{}_Hkv{}_d{}_N{}_p{}".format(*s[:6]))
+def test_random_shapes_bf16_out(cuda_lib, kernel, shape):
+    """The production output dtype (bf16, the one bench.py times) on every shape and both kernels:
+    out within 1 bf16 ulp of RNE(oracle) elementwise (R12), scores and slots as in fp32 mode (Alg. 1
+    P:539 o_t <- o_acc / l_acc, rounded once)."""
+    B, Hq, Hkv, d, N, pre, steps, split = shape
+    _need(kernel, Hq // Hkv, d)
+    wl = Workload("rand", B, Hq, Hkv, d, N, pre, steps)
+    cache, orc, syn = setup_pair(wl, kernel=kernel, split_tokens=split, seed=B * 37 + N, out_dtype="bf16")
+    run_lockstep(cache, orc, syn, steps, out_dtype="bf16")
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
 def test_maximum_budget(cuda_lib, kernel):
     """The largest budget the library builds (65,536 slots, lf_cache_create's limit): full cache,
     lockstep eviction steps (tcgen05 G=4: 16 CTAs x 4,096 tokens per unit; CUDA-core G=1)."""
@@ -152,14 +165,16 @@ def _embed(rows, d):
     return a
 
 
-@pytest.mark.parametrize("kernel", KERNELS)
-def test_gqa_worked_example_on_gpu(cuda_lib, kernel):
-    """C.3 #7 embedded in d=64 (zero padding leaves logits, L1 norms and outputs unchanged)."""
-    _need(kernel, 2, 64)
+@pytest.mark.parametrize("kernel,d", [("simt", 64), ("simt", 128), ("tcgen05", 128)])
+@pytest.mark.parametrize("out_dtype", ["f32", "bf16"])
+def test_gqa_worked_example_on_gpu(cuda_lib, kernel, d, out_dtype):
+    """C.3 #7 embedded in d = 64 / 128 (zero padding leaves logits, L1 norms and outputs unchanged);
+    at d = 128 it runs on the tcgen05 kernel (G = 2 in the M=128 x N=8 logit MMA).  bf16-out mode
+    must give the golden outputs rounded once to bf16."""
+    _need(kernel, 2, d)
     from paper_2603_11504_b200 import Cache
     g = json.load(open(os.path.join(GOLD, "gqa_worked_example.json")))
-    d = 64
-    cache = Cache(1, 2, 1, d, 3, kernel=kernel, softmax_scale=math.log(2.0))
+    cache = Cache(1, 2, 1, d, 3, kernel=kernel, softmax_scale=math.log(2.0), out_dtype=out_dtype)
     K = bf16(_embed(g["K"], d))[None].cuda()
     V = bf16(_embed(g["V"], d))[None].cuda()
     cache.prefill(0, K, V)
@@ -169,7 +184,11 @@ def test_gqa_worked_example_on_gpu(cuda_lib, kernel):
     out, slot, scores = cache.new_outputs(with_scores=True)
     cache.decode_step(q, kn, vn, out, slot, scores)
     torch.cuda.synchronize()
-    np.testing.assert_allclose(out[0, :, :2].cpu().numpy(), g["out"], rtol=1e-6, atol=1e-6)
+    want = np.asarray(g["out"], dtype=np.float64)
+    if out_dtype == "bf16":   # rounded once, RNE (R10/R12): 0.6 -> 0.6015625
+        want = torch.tensor(want, dtype=torch.float32).to(torch.bfloat16).double().numpy()
+    np.testing.assert_allclose(out[0, :, :2].double().cpu().numpy(), want, rtol=1e-6, atol=1e-6)
+    assert float(out[0, :, 2:].float().abs().max()) == 0.0
     np.testing.assert_allclose(scores[0, 0].cpu().numpy(), g["scores"], rtol=1e-6)
     assert int(slot[0, 0]) == g["slot"]
     Kc, Vc, nv = cache.views()
@@ -288,14 +307,15 @@ def test_q7_full_trajectory(cuda_lib):
 
 # --- full-size configs in the bench's launch configuration: sampled units ---------------------
 
+@pytest.mark.parametrize("out_dtype", ["f32", "bf16"])
 @pytest.mark.parametrize("tag", ["q3", "r"])
-def test_full_size_sampled_units(cuda_lib, tag):
-    """BASELINE configs[2]/[3] at full size, cache full (steady state), the plan bench.py uses:
-    every unit is checked for the one-slot-changes invariant; 12 sampled units are checked
-    element by element against the oracle (their K/V/q come from the seeded generator)."""
+def test_full_size_sampled_units(cuda_lib, tag, out_dtype):
+    """BASELINE configs[2]/[3] at full size, cache full (steady state), the plan and output dtype
+    bench.py uses (bf16): every unit is checked for the one-slot-changes invariant; 12 sampled units
+    are checked element by element against the oracle (their K/V/q come from the seeded generator)."""
     from paper_2603_11504_b200 import Cache
     wl = CONFIGS[tag]
-    cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype="f32")
+    cache = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype)
     K, V, nv = cache.views()
     k0, v0 = random_cache(wl.B, wl.Hkv, wl.N, wl.d, seed=11, device="cuda")
     K.copy_(k0)
@@ -325,7 +345,7 @@ def test_full_size_sampled_units(cuda_lib, tag):
     for (b, h) in units:
         Kb, Vb = host[(b, h)]
         r = oracle.unit_attend(qh[b, h * wl.G:(h + 1) * wl.G], Kb, Vb, knh[b, h], vnh[b, h])
-        check_out(out[b, h * wl.G:(h + 1) * wl.G].cpu().double().numpy(), r["out"], "f32", st)
+        check_out(out[b, h * wl.G:(h + 1) * wl.G].cpu().double().numpy(), r["out"], out_dtype, st)
         sc = scores[b, h].cpu().numpy().astype(np.float64)
         assert np.all(np.abs(sc - r["scores"]) <= 1e-4 * r["scores"] + 1e-30)
         s = int(slot[b, h])

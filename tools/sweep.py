@@ -49,6 +49,7 @@ for N in map(int, args.budgets.split(",")):
         K, V, nv = cache.views()
         k0, v0 = random_cache(B, wl.Hkv, N, wl.d, device="cuda")
         K.copy_(k0); V.copy_(v0); nv.fill_(N)
+        torch.cuda.synchronize()   # the decode steps below run on another stream
         del k0, v0
         syn = Synth(wl, device="cuda")
         pool = [syn.step() for _ in range(4)]
@@ -67,6 +68,7 @@ for N in map(int, args.budgets.split(",")):
             K2, V2, nv2 = c2.views()
             K2.copy_(K); V2.copy_(V); nv2.copy_(nv)
             layers.append(c2)
+        torch.cuda.synchronize()   # copies on the default stream before the steps on `st`
         tl["layers"] = time.time() - t0
         steps = max(3, min(args.steps, 2000 // max(L, 1)))   # bounded graph size (<= ~2000 launches)
         if L == 0:
