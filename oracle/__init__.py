@@ -54,6 +54,8 @@ def _load():
             lib.lfo_step_deferred.restype = i
             lib.lfo_snapkv_select.argtypes = [i, i, i, i, i, i, dbl, P, P, P, P, P]
             lib.lfo_snapkv_select.restype = i
+            lib.lfo_exact_objective.argtypes = [i, i, i, dbl, P, P, P, P, P, P]
+            lib.lfo_exact_objective.restype = i
             _lib = lib
     return _lib
 
@@ -137,6 +139,7 @@ class OracleCache:
         self.K[b, :, :n] = k
         self.V[b, :, :n] = v
         self.n_valid[b, :] = n
+        self.pend[b, :] = -1   # deferred modes: no victim chosen yet for this sequence (R26)
 
     def compute(self, q, k_new, v_new, want_scores=True):
         """Same-step mode (R1), no mutation.  Returns (out fp64 [B][Hq][d], slot int32 [B][Hkv],
@@ -200,6 +203,26 @@ def snapkv_select(q_obs, K, budget, pool_kernel=7, scale=None):
     if r < 0:
         raise OracleError(f"lfo_snapkv_select failed: {r}")
     return dict(kept=kept, score=score[:n - w], pooled=pooled[:n - w])
+
+
+def exact_objective(q, K, V, k_new=None, v_new=None, scale=None):
+    """NEXT-f4 by brute force (Eq. 3's right-hand side with the current query): for
+    every cached token i, the unit re-attended without it; E_i = mean_g ||o_g - o_g^(\\i)||^2.
+    q: uint16 [G][d]; K, V: uint16 [n][d]; k_new/v_new: uint16 [d] or None.  Returns E fp64 [n]."""
+    lib = _load()
+    q = _u16(q)
+    G, d = q.shape
+    K = _u16(K).reshape(-1, d)
+    V = _u16(V).reshape(-1, d)
+    n = K.shape[0]
+    kn = None if k_new is None else _u16(k_new).reshape(d)
+    vn = None if v_new is None else _u16(v_new).reshape(d)
+    sc = (1.0 / np.sqrt(d)) if scale is None else float(scale)
+    E = np.zeros((max(n, 1),), np.float64)
+    r = lib.lfo_exact_objective(G, d, n, sc, _p(q), _p(K), _p(V), _p(kn), _p(vn), _p(E))
+    if r:
+        raise OracleError(f"lfo_exact_objective failed: {r}")
+    return E[:n]
 
 
 def bf16_bits_to_f64(a) -> np.ndarray:

@@ -328,3 +328,43 @@ int lfo_snapkv_select(int G, int d, int n, int w, int ks, int budget, double sca
     free(score); free(pooled); free(s); free(taken);
     return o;
 }
+
+/* ------------------------------------------------------------------------- */
+/* NEXT-f4: the eviction objective itself, by brute force (Eq. 3's right-hand side, P:110:
+ * ||o_t - o_t^(\i)||^2 with the current query, "computed without the key-value pair of token
+ * t_i").  For every cached candidate i < n the unit is re-attended from scratch over the
+ * cache without row i (plus the current token, R1), with lfo_unit_attend, and
+ *   E_i = (1/G) sum_g sum_l (o_g[l] - o_g^(\i)[l])^2         (mean over the group, R2/R25).
+ * No closed form is used (App. A's exact remainder is only a check of this in the tests).
+ *   E [n] fp64.  returns 0, or < 0 on error (n < 2: nothing to evict and keep attending). */
+int lfo_exact_objective(int G, int d, int n, double scale,
+                        const uint16_t *q, const uint16_t *K, const uint16_t *V,
+                        const uint16_t *k_new, const uint16_t *v_new, double *E) {
+    if (n < 1) return -1;
+    double *o = (double *)malloc(sizeof(double) * (size_t)G * (size_t)d);
+    double *oi = (double *)malloc(sizeof(double) * (size_t)G * (size_t)d);
+    uint16_t *Ki = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 1 ? n - 1 : 1) * (size_t)d);
+    uint16_t *Vi = (uint16_t *)malloc(sizeof(uint16_t) * (size_t)(n > 1 ? n - 1 : 1) * (size_t)d);
+    if (!o || !oi || !Ki || !Vi) { free(o); free(oi); free(Ki); free(Vi); return -3; }
+    int r = lfo_unit_attend(G, d, n, scale, q, K, V, k_new, v_new, o, NULL, NULL, NULL, NULL);
+    for (int i = 0; i < n && r >= -1; ++i) {
+        /* the cache without row i, rows in their original order */
+        int w = 0;
+        for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            memcpy(Ki + (size_t)w * d, K + (size_t)j * d, sizeof(uint16_t) * (size_t)d);
+            memcpy(Vi + (size_t)w * d, V + (size_t)j * d, sizeof(uint16_t) * (size_t)d);
+            ++w;
+        }
+        r = lfo_unit_attend(G, d, n - 1, scale, q, Ki, Vi, k_new, v_new, oi, NULL, NULL, NULL, NULL);
+        double acc = 0.0;
+        for (int g = 0; g < G; ++g)
+            for (int l = 0; l < d; ++l) {
+                double dl = o[(size_t)g * d + l] - oi[(size_t)g * d + l];
+                acc += dl * dl;
+            }
+        E[i] = acc / (double)G;
+    }
+    free(o); free(oi); free(Ki); free(Vi);
+    return r < -1 ? r : 0;
+}

@@ -149,7 +149,10 @@ __device__ __forceinline__ int solo_items(const StepParams& p, int cid, int s, i
 // (cluster cid takes solo_units + cid, + C, ...): balanced tails without paying the exchange on
 // every unit.  Which units are whole is part of the plan of the plan_batch problem (lf_runtime.cu),
 // so a shard computes every unit exactly as the one-GPU cache does.
-__device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int s, int C, int i, int R) {
+__device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int s, int C, int i) {
+    // recomputed per call: a CTA-wide variable live across the warp roles moved the MMA issuer's
+    // descriptor arithmetic off the uniform datapath (R2UR per MMA, -3 % on f1/q3)
+    const int R = solo_items(p, cid, s, C);
     UnitInfo x;
     const int S = p.splits, P = C * S;
     bool split;
@@ -218,7 +221,6 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     const int s = (int)cluster.block_rank();
     const int cid = blockIdx.x / S;
     const int C = a.clusters;
-    const int R = solo_items(p, cid, s, C);   // whole units of this CTA (its first R items)
     volatile int* nsm = (volatile int*)(smem + so.nsm);
 
     if (tid == 0) {
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     }
 #endif
     if (tid == 64) {   // L2 warm-up of the first item's operands; safe before the PDL wait (L2 is coherent)
-        const UnitInfo x = item_base(p, cid, s, C, 0, R);
+        const UnitInfo x = item_base(p, cid, s, C, 0);
         if (x.valid) {
             const int u = x.u;
             ptx::bulk_prefetch_l2(p.n_valid + (u & ~3), 16);
@@ -299,7 +301,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             for (int i = 0;; ++i, ++qi) {
                 // every global read of the item goes out at once (Q rows, fill state):
                 // one L2 round trip instead of a chain of them before the first MMA
-                UnitInfo x = item_base(p, cid, s, C, i, R);
+                UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
                 if (lane == 0) LF_PROG(0, ((unsigned long long)i << 32) | it);
                 const int u = x.u;
@@ -351,7 +353,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         } else {
             uint32_t it = 0, qi = 0;
             for (int i = 0;; ++i, ++qi) {
-                UnitInfo x = item_base(p, cid, s, C, i, R);
+                UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
                 if (lane == 0) LF_PROG(0, ((unsigned long long)i << 32) | it);
                 set_fill(x, __ldcg(p.n_valid + x.u));
@@ -400,12 +402,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         if (lane == 0) {
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
-            uint32_t it = 0, ui = 0;
-            uint32_t pc[kNG];   // V tiles handed to each softmax group so far (PREADY / PFREE phases)
-#pragma unroll
-            for (int g = 0; g < kNG; ++g) pc[g] = 0;
+            uint32_t it = 0, pi = 0, ui = 0;
             for (int i = 0;; ++i, ++ui) {
-                UnitInfo x = item_base(p, cid, s, C, i, R);
+                UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
                 ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
                 set_fill(x, nsm[i & 7]);
@@ -435,18 +434,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::mma_commit(BAR(QFREE + par));
                 ptx::mma_commit(BAR(KDONE + par));
                 const uint32_t oreg = tmem + (par ^ 1u) * RC;
-                for (int t = 0; t < x.ntiles; ++t, ++it) {                 // O^T += V^T . P^T
+                for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    // tile t of a unit always goes to softmax group t % kNG, so each group's partial
-                    // Z sums a fixed set of the unit's tiles: the unit's arithmetic does not depend on
-                    // which units the CTA computed before it (shard invariance)
-                    const int pb = t % kNG;
-                    uint32_t k = 0;
-#pragma unroll
-                    for (int g = 0; g < kNG; ++g)
-                        if (g == pb) k = pc[g]++;
-                    ptx::mbar_wait(BAR(PREADY + pb), k & 1u);
+                    const int pb = pi % kNG;
+                    ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
@@ -516,13 +508,30 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             return best;
         };
-        uint32_t it = 0, gc = 0, ui = 0, xi = 0;   // gc: V tiles this softmax group handled so far
+        uint32_t it = 0, pi = 0, ui = 0, xi = 0;
+        // the CTA's max and denominator of head g from the per-warp partials in red[]: the max is exact
+        // in any order; Z adds the warps' partials subset by subset (tiles s, s + kNG, ... of the unit
+        // live in group (g0 + s) % kNG), a fixed fp32 order per unit whatever units the CTA computed
+        // before -- so a shard computes every unit bit-identically to the one-GPU run
+        auto unit_max = [&](int g) {
+            float mm = red[g];
+            for (int w = 1; w < 4 * kNG; ++w) mm = fmaxf(mm, red[w * 16 + g]);
+            return mm;
+        };
+        auto unit_z = [&](int g, int g0) {
+            float zz = 0.f;
+            for (int sg = 0; sg < kNG; ++sg) {
+                const int w0 = ((g0 + sg) % kNG) * 4;
+                for (int q = 0; q < 4; ++q) zz += red[kNG * 64 + (w0 + q) * 16 + g];
+            }
+            return zz;
+        };
         for (int i = 0;; ++i, ++ui) {
             UnitInfo x;
             uint4* kvn = (uint4*)(smem + so.kvn);
             if constexpr (kLat) {
                 // all global reads of the item at once: fill state, k*/v* rows, the x* operands
-                x = item_base(p, cid, s, C, i, R);
+                x = item_base(p, cid, s, C, i);
                 if (sidx == 0 && i == 0) LF_EVENT(0, 20);
                 if (!x.valid) break;
                 const int u = x.u;
@@ -554,7 +563,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     if (xch == 0 && xg < G) xs[xg] = p.deferred ? -INFINITY : acc * sl2;
                 }
             } else {
-                x = item_base(p, cid, s, C, i, R);
+                x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
                 const int u = x.u;
                 // stage the current token's k*, v* rows (combine + eviction write read them later)
@@ -586,7 +595,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             // latency variant, one tile per CTA: its V tile lands with (or before) K, so lambda_j and
             // the zeroing of rows past n happen while the QK MMA runs (PREADY still follows them)
             const bool lam_first = kLat && x.ntiles == 1;
-            if (lam_first && grp == 0) {
+            if (lam_first && (int)(pi % kNG) == grp) {
                 const uint32_t iv = it + 1;
                 const int st = iv % ST;
                 ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);
@@ -646,11 +655,16 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             float z[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) z[g] = 0.f;
-            for (int t = grp; t < x.ntiles; t += kNG, ++gc) {   // tile t -> group t % kNG (fixed per unit)
-                const int pb = grp;
+            // V tiles go round-robin over the groups across units (c = the CTA's tile count), so the
+            // tiles t = s, s + kNG, ... of this unit (subset s) are all handled by group (pi + s) % kNG
+            const int g0 = (int)(pi % kNG);   // group of subset 0 in this unit
+            for (int t = 0; t < x.ntiles; ++t) {
+                const uint32_t c = pi + t;
+                if ((int)(c % kNG) != grp) continue;
+                const int pb = c % kNG;
                 uint32_t r[8];
                 ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::mbar_wait(BAR(PFREE + pb), (gc & 1u) ^ 1u);
+                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNG) & 1u) ^ 1u);
                 ptx::tmem_ld_wait();
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
@@ -695,6 +709,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
                 if (lane == 0 && q4 == 0) LF_TILE_EVENT(ui, 33, t);
             }
+            pi += x.ntiles;
             it += 2 * x.ntiles;
 #pragma unroll
             for (int g = 0; g < GP; ++g) {
@@ -711,11 +726,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 ptx::named_bar_sync(1, kNS);                                  // red[] complete
                 if (sidx < G) {
                     const int g = sidx;
-                    float mm = red[g], zz = red[kNG * 64 + g];
-                    for (int w = 1; w < 4 * kNG; ++w) {
-                        mm = fmaxf(mm, red[w * 16 + g]);
-                        zz += red[kNG * 64 + w * 16 + g];
-                    }
+                    const float mm = unit_max(g);
+                    const float zz = unit_z(g, g0);
                     const float M = fmaxf(mm, xs[g]);
                     const float f = ptx::ex2_approx(mm - M);
                     const float Z = zz * f + ptx::ex2_approx(xs[g] - M);
@@ -821,11 +833,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (sidx == 0) LF_EVENT(ui, 10);
             if (sidx < S * G) {                                         // (m_g, Z_g) -> rank t
                 const int t = sidx / G, g = sidx % G;
-                float mm = red[g], zz = red[kNG * 64 + g];
-                for (int w = 1; w < 4 * kNG; ++w) {
-                    mm = fmaxf(mm, red[w * 16 + g]);
-                    zz += red[kNG * 64 + w * 16 + g];
-                }
+                const float mm = unit_max(g);
+                const float zz = unit_z(g, g0);
                 ptx::st_async_f32x2(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, mz) + 8 * (s * 16 + g), t), mm, zz,
                                     ptx::mapa(xr_local, t));
             }

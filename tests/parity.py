@@ -2,7 +2,8 @@
 
 Tolerances (reading R12, from BASELINE.json north_star):
   out     fp32-out mode: normwise per (sequence, q head) row, max_l|o - o^| / max_l|o^| <= 2e-3
-          bf16-out mode: |o_bf16 - RNE_bf16(o^)| <= 1 bf16 ulp of o^ (elementwise)
+          bf16-out mode: every element is the single RNE rounding of a value within 1e-4 x max|o^_row|
+          of o^: |o_bf16 - o^| <= ulp(o_bf16)/2 + ulp(o^)/2 + 1e-4 max|o^_row| (elementwise)
   scores  |I - I^| <= 1e-4 I^ + 1e-30 elementwise on valid slots; +inf on invalid slots
   slot    identical, except an accepted near-tie: I^_slot <= (1 + 1e-4) min_k I^_k + 1e-30;
           then the oracle adopts the GPU's slot (both are correct, R13) so the two caches stay
@@ -19,6 +20,7 @@ import oracle
 from lf_synth import Synth, Workload, bits
 
 OUT_TOL = 2e-3
+BF16_FP32_SLACK = 1e-4   # bf16 out: fp32-path error allowed before the single rounding (R12)
 SCORE_RTOL = 1e-4
 SCORE_ATOL = 1e-30
 
@@ -30,6 +32,7 @@ class Stats:
     max_score_err: float = 0.0
     adoptions: int = 0
     evictions: int = 0
+    bf16_exact_frac: float = 1.0   # bf16 out: fraction of elements equal to RNE(oracle)
 
 
 def bf16_ulp(x: np.ndarray) -> np.ndarray:
@@ -46,10 +49,20 @@ def check_out(o_gpu: np.ndarray, o_ref: np.ndarray, out_dtype: str, stats: Stats
         stats.max_out_err = max(stats.max_out_err, float(err.max()))
         assert err.max() <= OUT_TOL, f"out normwise error {err.max():.3e} > {OUT_TOL}"
     else:
+        # bf16 out = RNE of the kernel's fp32 result, rounded ONCE: each element must equal the bf16
+        # rounding of some value within BF16_FP32_SLACK * max|o^_row| of the exact o^ (R12):
+        #   |o_bf16 - o^| <= ulp(o_bf16)/2 + ulp(o^)/2 + slack * max|o^_row|
+        # i.e. RNE(o^) or its neighbour where o^ sits within the fp32 error of a rounding boundary,
+        # and an absolute fp32-size allowance for elements near zero (their ulp is tiny).
+        den = np.abs(o_ref).max(axis=-1, keepdims=True)
+        excess = np.abs(o_gpu - o_ref) - 0.5 * bf16_ulp(o_gpu) - 0.5 * bf16_ulp(o_ref)
+        rel = np.maximum(excess, 0.0) / np.maximum(den, 1e-300)
+        stats.max_out_err = max(stats.max_out_err, float(rel.max()))
+        bad = rel > BF16_FP32_SLACK
+        assert not bad.any(), (f"bf16 out: not a single rounding of a value within {BF16_FP32_SLACK} (normwise) "
+                               f"of the exact output at {np.argwhere(bad)[:5]} (excess {rel.max():.3e})")
         ref_bf16 = torch.from_numpy(o_ref).to(torch.float32).to(torch.bfloat16).double().numpy()
-        d = np.abs(o_gpu - ref_bf16)
-        ok = d <= bf16_ulp(o_ref) * 1.0000001
-        assert ok.all(), f"bf16 out off by > 1 ulp at {np.argwhere(~ok)[:5]}"
+        stats.bf16_exact_frac = float((o_gpu == ref_bf16).mean())
 
 
 def check_scores(sc_gpu: np.ndarray, sc_ref: np.ndarray, n_valid: np.ndarray, stats: Stats):

@@ -83,3 +83,35 @@ def test_deferred_cross_mode_identity_on_gpu(cuda_lib):
             rb = [bytes(r) for r in bits(Kb[s, h]).view(np.uint8).reshape(N, -1)]
             del rb[pend[s, h]]
             assert ra == set(rb)
+
+
+@pytest.mark.parametrize("mode", ["deferred", "deferred_exclude_newest"])
+def test_deferred_full_prefill_is_a_protocol_error(cuda_lib, mode):
+    """R26: in the Fig. 2-literal modes a step's token covers the slot chosen at the PREVIOUS step
+    (P:152).  A sequence prefilled to the whole budget has none, so lf_decode_step refuses it
+    (LF_ERR_INVALID_ARGUMENT, before any launch) -- as the oracle's lfo_step_deferred does -- and a
+    re-prefill below the budget clears the state (and the stale pending victim of the sequence)."""
+    from paper_2603_11504_b200 import Cache, LFError
+    B, Hq, Hkv, d, N = 2, 8, 2, 128, 64
+    wl = Workload("defer_full", B, Hq, Hkv, d, N, N, 1)
+    syn = Synth(wl, seed=3)
+    cache = Cache(B, Hq, Hkv, d, N, mode=mode)
+    orc = oracle.OracleCache(B, Hq, Hkv, d, N)
+    K, V = syn.prefill()
+    cache.prefill(0, K[0, :, :N - 4].cuda(), V[0, :, :N - 4].cuda())
+    cache.prefill(1, K[1].cuda(), V[1].cuda())                       # full: no victim chosen yet
+    orc.prefill(0, bits(K[0, :, :N - 4]), bits(V[0, :, :N - 4]))
+    orc.prefill(1, bits(K[1]), bits(V[1]))
+    q, kn, vn = syn.step()
+    out, slot, _ = cache.new_outputs()
+    with pytest.raises(LFError) as e:
+        cache.decode_step(q.cuda(), kn.cuda(), vn.cuda(), out, slot)
+    assert e.value.status == 1 and "sequence 1" in str(e.value)
+    with pytest.raises(oracle.OracleError):
+        orc.step_deferred(bits(q), bits(kn), bits(vn), exclude_newest=mode.endswith("newest"))
+    # the pending victims were reset by the prefill
+    assert (cache.pending().cpu().numpy() == -1).all()
+    cache.prefill(1, K[1, :, :N - 1].cuda(), V[1, :, :N - 1].cuda())   # below the budget: fine again
+    cache.decode_step(q.cuda(), kn.cuda(), vn.cuda(), out, slot)
+    torch.cuda.synchronize()
+    assert slot.cpu().numpy().tolist() == [[N - 4] * Hkv, [N - 1] * Hkv]

@@ -1,5 +1,6 @@
-"""GPU diagnostics kernel (NEXT-f4) against the oracle: LongFlow victim, exact-objective victim
-(Eq. 3's right-hand side via App. A's exact remainder), remainder bound."""
+"""GPU diagnostics kernel (NEXT-f4) against the oracle: LongFlow victim, exact-objective victim (Eq. 3's
+right-hand side, which the kernel evaluates with App. A's exact remainder P:424-426 and the oracle by
+brute-force re-attention without each token), remainder bound."""
 import numpy as np
 import pytest
 import torch
@@ -32,10 +33,9 @@ def test_diag_matches_oracle(cuda_lib, G, d, N, pre):
         for h in range(Hkv):
             r = oracle.unit_attend(bits(q[b, h * G:(h + 1) * G]), bits(K[b, h]), bits(V[b, h]), bits(kn[b, h]),
                                    bits(vn[b, h]))
-            a = r["alpha"][:, :pre]
-            Vf = oracle.bf16_bits_to_f64(bits(V[b, h]))
-            dist2 = ((Vf[None, :, :] - r["out"][:, None, :]) ** 2).sum(-1)          # [G][n]
-            E = ((a / (1 - a)) ** 2 * dist2).mean(0)
+            # the exact objective by brute force: the unit re-attended without each token (oracle/)
+            E = oracle.exact_objective(bits(q[b, h * G:(h + 1) * G]), bits(K[b, h]), bits(V[b, h]),
+                                       bits(kn[b, h]), bits(vn[b, h]))
             lf, ex, rank = islot[b, h]
             assert lf == r["slot"] or _near(r["scores"], lf, r["slot"])
             assert ex == int(np.argmin(E)) or _near(E, ex, int(np.argmin(E)))

@@ -157,6 +157,32 @@ def test_spec_d1_worked_example_and_appendix_a():
     assert abs(2 * Vmax * a0 / (1 - a0) - g["remainder_bound_0"]) < 1e-15
 
 
+def test_exact_objective_d1_worked_example():
+    """NEXT-f4 oracle (brute-force re-attention, Eq. 3's right-hand side P:110) on the d=1 worked
+    example: ||o - o^(-i)||^2 = (0.75^2, 2.25^2) (the exact output changes), argmin 0 like the
+    LongFlow score."""
+    g = json.load(open(os.path.join(GOLD, "spec_d1_example.json")))
+    sc = _scale(g["scale"])
+    E = oracle.exact_objective(_b(g["q"]), _b(g["K"]), _b(g["V"]), scale=sc)
+    np.testing.assert_allclose(E, np.square(g["delta_o_all"]), rtol=0, atol=1e-14)
+    assert int(np.argmin(E)) == g["slot"]
+
+
+@pytest.mark.parametrize("G,d,n", [(1, 16, 9), (4, 32, 40), (7, 64, 25)])
+def test_exact_objective_matches_appendix_a_closed_form(G, d, n):
+    """The brute-force objective equals App. A's exact change (Delta o = alpha/(1-alpha)
+    (v_i - o), so ||Delta o||^2 = (alpha/(1-alpha))^2 ||v_i - o||^2), mean over the group (R25), on
+    random units with the current token attended -- two independent routes to the same number."""
+    rng = np.random.default_rng(G * 1000 + n)
+    q, K, V = _b(rng.standard_normal((G, d))), _b(rng.standard_normal((n, d))), _b(rng.standard_normal((n, d)))
+    kn, vn = _b(rng.standard_normal(d)), _b(rng.standard_normal(d))
+    E = oracle.exact_objective(q, K, V, kn, vn)
+    r = oracle.unit_attend(q, K, V, kn, vn)
+    a = r["alpha"][:, :n]
+    closed = ((a / (1 - a)) ** 2 * ((_f64(V)[None, :, :] - r["out"][:, None, :]) ** 2).sum(-1)).mean(0)
+    np.testing.assert_allclose(E, closed, rtol=1e-9, atol=1e-15)
+
+
 def test_gqa_worked_example():
     """C.3 #7: mean-over-group aggregation evicts slot 2 (max -> 1, head-0 only -> 0)."""
     g = json.load(open(os.path.join(GOLD, "gqa_worked_example.json")))
