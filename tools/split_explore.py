@@ -71,7 +71,7 @@ def measure(B, N, **kw):
 for pt in args.points.split(","):
     B, N = map(int, pt.split("x"))
     for S in map(int, args.splits.split(",")):
-        split = 0 if S == 0 else -(-N // S + 127) // 128 * 128
+        split = 0 if S == 0 else ((N + S - 1) // S + 127) // 128 * 128
         if S and -(-N // split) != S:
             continue
         for k in (map(int, args.ks.split(",")) if S else [0]):
@@ -80,6 +80,7 @@ for pt in args.points.split(","):
                 try:
                     rec = measure(B, N, **kw)
                 except LFError as e:
+                    print("no plan", B, N, kw, str(e)[:120], flush=True)
                     continue
                 print(json.dumps(rec), flush=True)
                 f.write(json.dumps(rec) + "\n")
