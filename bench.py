@@ -307,7 +307,8 @@ def config_of(args, wl, B_total, plan):
                   "solo_rounds": plan.get("solo_rounds", 0), "ctas_per_sm": 2 if plan.get("tmem_cols") == 256 else 1,
                   "latency_variant": plan.get("latency_variant", 0)})
         if args.gpus > 1 and args.scaling == "strong":
-            c["shard_plan"] = "plan of the global batch (plan_batch), bit-identical to one GPU"
+            c["shard_plan"] = (f"plan chosen for one of {args.gpus} shards and fixed for the global batch "
+                               f"(plan_batch, plan_shards): bit-identical to one GPU with the same plan")
     if getattr(args, "mode", "same_step") != "same_step":
         c["mode"] = args.mode
     return c
@@ -379,7 +380,8 @@ def main():
     onoff = {"auto": None, "on": True, "off": False}
     # strong scaling: this rank's shard is computed with the plan of the whole batch (bit-identical
     # to the one-GPU run); weak scaling: every rank holds a whole problem
-    shard_kw = dict(plan_batch=B_total, seq_offset=b0) if args.scaling == "strong" and args.gpus > 1 else {}
+    shard_kw = (dict(plan_batch=B_total, seq_offset=b0, plan_shards=args.gpus)
+                if args.scaling == "strong" and args.gpus > 1 else {})
     cache_kw = dict(out_dtype=args.out_dtype, kernel=args.kernel, split_tokens=args.split_tokens, device=local,
                     mode=args.mode, ctas_per_sm=args.ctas_per_sm, solo=onoff[args.solo],
                     latency_variant=onoff[args.latency_variant], **shard_kw)

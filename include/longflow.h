@@ -88,6 +88,11 @@ typedef struct {
      * the whole problem (plan_batch = batch, seq_offset = 0). */
     int32_t plan_batch;    /* 0, or >= seq_offset + batch                                        */
     int32_t seq_offset;    /* first sequence of this cache in the global batch (0 if plan_batch == 0) */
+    int32_t plan_shards;   /* 0/1, or P: the plan is chosen for ONE of P equal shards of plan_batch
+                              (the per-GPU work of a P-GPU deployment) and then fixed for every cache of
+                              that problem; it uses no whole-unit rounds, so every unit is split the same
+                              way whichever cache holds it.  A one-GPU cache of the whole batch with the
+                              same plan_shards reproduces the P-GPU run bit for bit.                   */
     /* Plan overrides (tests and measurements; 0 = automatic).  They change which CTAs compute a
      * unit, never what is computed. */
     int32_t ctas_per_sm;      /* tcgen05: 1 (three softmax groups, 512 TMEM columns) or 2 (one group, 256) */

@@ -40,6 +40,7 @@ class CacheConfig(ctypes.Structure):
                 ("head_dim", ctypes.c_int32), ("budget", ctypes.c_int32), ("out_dtype", ctypes.c_int32),
                 ("softmax_scale", ctypes.c_float), ("mode", ctypes.c_int32), ("kernel", ctypes.c_int32),
                 ("split_tokens", ctypes.c_int32), ("plan_batch", ctypes.c_int32), ("seq_offset", ctypes.c_int32),
+                ("plan_shards", ctypes.c_int32),
                 ("ctas_per_sm", ctypes.c_int32), ("solo", ctypes.c_int32), ("latency_variant", ctypes.c_int32)]
 
 
@@ -117,11 +118,11 @@ _LAT = {None: 0, "auto": 0, False: 1, True: 2}
 
 
 def make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32", softmax_scale=0.0,
-                kernel="auto", split_tokens=0, mode="same_step", plan_batch=0, seq_offset=0, ctas_per_sm=0,
-                solo=None, latency_variant=None) -> CacheConfig:
+                kernel="auto", split_tokens=0, mode="same_step", plan_batch=0, seq_offset=0, plan_shards=0,
+                ctas_per_sm=0, solo=None, latency_variant=None) -> CacheConfig:
     return CacheConfig(batch, num_q_heads, num_kv_heads, head_dim, budget, DTYPES[out_dtype],
                        float(softmax_scale), MODES[mode], KERNELS[kernel], split_tokens, plan_batch, seq_offset,
-                       ctas_per_sm, _SOLO[solo], _LAT[latency_variant])
+                       plan_shards, ctas_per_sm, _SOLO[solo], _LAT[latency_variant])
 
 
 def cache_bytes(cfg: CacheConfig) -> int:
@@ -135,16 +136,18 @@ class Cache:
 
     By default the slab is a torch uint8 CUDA tensor passed as caller-owned device memory
     (`library_owned=True` makes the library do its single cudaMalloc instead).  A rank's shard of a
-    global batch passes plan_batch (the global batch) and seq_offset (its first sequence) so every
-    unit is computed exactly as on one GPU; ctas_per_sm / solo / latency_variant override the plan.
+    global batch passes plan_batch (the global batch), seq_offset (its first sequence) and plan_shards
+    (the number of shards) so every unit is computed exactly as a one-GPU cache of the whole batch with
+    the same plan_shards computes it; ctas_per_sm / solo / latency_variant override the plan.
     """
 
     def __init__(self, batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype="f32",
                  softmax_scale=0.0, kernel="auto", split_tokens=0, device=0, library_owned=False,
-                 mode="same_step", plan_batch=0, seq_offset=0, ctas_per_sm=0, solo=None, latency_variant=None):
+                 mode="same_step", plan_batch=0, seq_offset=0, plan_shards=0, ctas_per_sm=0, solo=None,
+                 latency_variant=None):
         lib = load()
         self.cfg = make_config(batch, num_q_heads, num_kv_heads, head_dim, budget, out_dtype, softmax_scale,
-                               kernel, split_tokens, mode, plan_batch, seq_offset, ctas_per_sm, solo,
+                               kernel, split_tokens, mode, plan_batch, seq_offset, plan_shards, ctas_per_sm, solo,
                                latency_variant)
         self.B, self.Hq, self.Hkv, self.d, self.N = batch, num_q_heads, num_kv_heads, head_dim, budget
         self.G = num_q_heads // num_kv_heads

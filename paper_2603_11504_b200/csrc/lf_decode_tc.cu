@@ -1159,6 +1159,35 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 1 && G <= 8; }
 // with the measured unit-boundary overheads in streamed tokens (ovh_1 ~ 128 alone, ovh_S ~ 1024
 // with the cross-CTA exchange).  Solo rounds process whole units per CTA (no exchange); the
 // remaining units are split S ways, which balances the tail.
+// Round model of a plan's step time (us) in the HBM regime, fitted to a measured exploration of the
+// plan space on B200 (profiles/r02_split_explore.jsonl: S = 1..8 x k x solo at 8 mid-size sweep points,
+// plus the r02 budget sweep; picks within 0-4 % of the best measured plan there): in every round the A
+// active CTAs each stream `tokens` (512 B each, K + V); the round lasts the longer of the HBM time
+// A * bytes / BW and one CTA's streaming time bytes / rho_k (rho_1 = 48 GB/s with three softmax groups,
+// rho_2 = 26 GB/s with one), plus the unit-boundary overhead (1 us for whole units, 3 us for split units:
+// the part of the cross-CTA exchange the next unit's K pass does not hide).  It sees what the token
+// proxy below does not: a last round with few active CTAs, and clusters the GPCs cannot pack (S = 4:
+// 33 clusters = 132 SMs), which is why mid-size grids (B = 16-32) prefer S = 5 or 6 at two CTAs per SM.
+static double stream_cost_us(long long units, int S, int C, int chunk, int N, long long R, int k) {
+    const double bw = 6.8e12, rho = k == 1 ? 48e9 : 26e9, ovh1 = 1.0, ovhS = 3.0;
+    const long long P = (long long)C * S;
+    long long rem = units;
+    double t = 0.0;
+    for (long long r = 0; r < R && rem > 0; ++r) {
+        const long long A = rem < P ? rem : P;
+        const double by = (double)N * 512.0;
+        t += fmax((double)A * by / bw, by / rho) * 1e6 + ovh1;
+        rem -= A;
+    }
+    while (rem > 0) {
+        const long long c = rem < C ? rem : C;
+        const double by = (double)(chunk < N ? chunk : N) * 512.0;
+        t += fmax((double)(c * S) * by / bw, by / rho) * 1e6 + (S > 1 ? ovhS : ovh1);
+        rem -= c;
+    }
+    return t;
+}
+
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, const PlanForce& force) {
     (void)d;
     Plan best;
@@ -1172,8 +1201,17 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
     best.tmem_cols = 0;
     best.solo_rounds = 0;
     const int Nr = (N + 127) / 128 * 128;
-    long long best_cost = -1;
-    for (int S = 1; S <= 16; S *= 2) {
+    // Two regimes.  Steps that move >= 64 MB are HBM streams: the round model (stream_cost_us) over
+    // every cluster size S = 1..16.  Smaller steps are latency chains (q7, small sweep points): the
+    // token proxy below, tuned with the trace over power-of-two S in round 1.
+    // Above 16 GB per step the round model's 9-CTA two-per-SM picks measured worse than the token
+    // proxy's S = 4 in long runs (512 x 16384: 0.87 vs 0.98 of the copy peak; 256 x 16384: 2.92 vs
+    // 2.72 ms under the power cap, profiles/r02_ab_planner.txt), so the proxy keeps the largest steps.
+    const double step_bytes = (double)units * (double)N * 512.0;
+    const bool hbm_regime = step_bytes >= 64e6 && step_bytes <= 16e9;
+    double best_cost = -1;
+    for (int S = 1; S <= 16; ++S) {
+        if (!hbm_regime && (S & (S - 1))) continue;
         const int chunk = split_tokens > 0 ? split_tokens : ((Nr + S - 1) / S + 127) / 128 * 128;
         const int splits = (N + chunk - 1) / chunk;
         if (splits != S && !(split_tokens > 0 && S == 1)) continue;   // each S once
@@ -1182,6 +1220,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
             if (force.ctas_per_sm && k != force.ctas_per_sm) continue;
             for (int solo = 0; solo <= 1; ++solo) {
                 if (force.solo && solo != force.solo - 1) continue;
+                if (solo && force.no_solo) continue;
                 if (solo && (splits == 1 || Nr > kMaxChunk)) continue;
                 const int hold = solo ? max(Nr, chunk) : chunk;
                 const int tiles = (hold + 127) / 128;
@@ -1210,18 +1249,20 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
                 if (k == 2) C *= 2;
                 if (C <= 0) continue;
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
-                long long cost, R = 0;
+                double cost;
+                long long R = 0;
                 int Cu;
                 if (solo) {
                     R = units / ((long long)C * splits);
                     if (R == 0) continue;
                     const long long rem = units - R * C * splits;
                     Cu = C;
-                    cost = R * ((long long)k * Nr + ovh1 / k) + ((rem + C - 1) / C) * ((long long)k * chunk + ovhS / k);
+                    cost = (double)(R * ((long long)k * Nr + ovh1 / k) + ((rem + C - 1) / C) * ((long long)k * chunk + ovhS / k));
                 } else {
                     Cu = C < units ? C : units;
-                    cost = ((units + Cu - 1) / Cu) * ((long long)k * chunk + ovhS / k);
+                    cost = (double)(((units + Cu - 1) / Cu) * ((long long)k * chunk + ovhS / k));
                 }
+                if (hbm_regime) cost = stream_cost_us(units, splits, C, chunk, N, R, k);
                 if (best_cost < 0 || cost < best_cost) {
                     best_cost = cost;
                     best.splits = splits;

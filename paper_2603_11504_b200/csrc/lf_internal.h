@@ -43,6 +43,7 @@ struct PlanForce {
     int32_t ctas_per_sm;
     int32_t solo;
     int32_t lat;
+    int32_t no_solo;   // plan_shards > 1: every unit split the same way in every shard (no solo rounds)
 };
 
 struct Plan {

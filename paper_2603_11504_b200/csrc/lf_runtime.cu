@@ -88,6 +88,10 @@ lf_status validate(const lf_cache_config* c) {
     if (c->plan_batch > 0 && (long long)c->seq_offset + c->batch > c->plan_batch)
         return fail(LF_ERR_INVALID_ARGUMENT, "sequences [%d, %d) exceed plan_batch %d", c->seq_offset,
                     c->seq_offset + c->batch, c->plan_batch);
+    if (c->plan_shards < 0 || c->plan_shards > 4096)
+        return fail(LF_ERR_INVALID_ARGUMENT, "plan_shards %d out of [0, 4096]", c->plan_shards);
+    if (c->plan_shards > 1 && c->solo == 2)
+        return fail(LF_ERR_INVALID_ARGUMENT, "plan_shards > 1 plans have no whole-unit rounds (solo = 2)");
     if (c->ctas_per_sm < 0 || c->ctas_per_sm > 2 || c->solo < 0 || c->solo > 2 || c->latency_variant < 0 ||
         c->latency_variant > 2)
         return fail(LF_ERR_INVALID_ARGUMENT, "plan overrides must be 0 (automatic), 1 or 2");
@@ -181,6 +185,8 @@ lf_status make_plan(lf_cache* c) {
     int G = g.num_q_heads / g.num_kv_heads;
     const int units = g.batch * g.num_kv_heads;
     const int plan_units = (g.plan_batch > 0 ? g.plan_batch : g.batch) * g.num_kv_heads;
+    const int shards = g.plan_shards > 1 ? g.plan_shards : 1;
+    const int shard_units = (plan_units + shards - 1) / shards;   // the plan is chosen for one shard
     bool want_tc = g.kernel == LF_KERNEL_TCGEN05 ||
                    (g.kernel == LF_KERNEL_AUTO && lf::tc_supported(G, g.head_dim));
     c->solo_units = 0;
@@ -190,16 +196,16 @@ lf_status make_plan(lf_cache* c) {
         // The plan depends only on the problem shape, the overrides and the device (occupancy queries:
         // ~1 ms per plan), and a model creates one cache per layer with the same shape: memoise it.
         struct Key {
-            int dev, units, G, d, N, split, sms, k, solo, lat;
+            int dev, units, G, d, N, split, sms, k, solo, lat, shards;
             bool operator==(const Key& o) const {
                 return dev == o.dev && units == o.units && G == o.G && d == o.d && N == o.N && split == o.split &&
-                       sms == o.sms && k == o.k && solo == o.solo && lat == o.lat;
+                       sms == o.sms && k == o.k && solo == o.solo && lat == o.lat && shards == o.shards;
             }
         };
         static std::mutex mu;
         static std::vector<std::pair<Key, lf::Plan>> memo;
-        const Key k{c->device, plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms,
-                    g.ctas_per_sm, g.solo, g.latency_variant};
+        const Key k{c->device, shard_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms,
+                    g.ctas_per_sm, g.solo, g.latency_variant, shards > 1};
         bool hit = false;
         {
             std::lock_guard<std::mutex> lock(mu);
@@ -211,8 +217,8 @@ lf_status make_plan(lf_cache* c) {
                 }
         }
         if (!hit) {
-            const lf::PlanForce force{g.ctas_per_sm, g.solo, g.latency_variant};
-            c->plan = lf::tc_plan(plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms, force);
+            const lf::PlanForce force{g.ctas_per_sm, g.solo, g.latency_variant, shards > 1};
+            c->plan = lf::tc_plan(shard_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms, force);
             if (c->plan.splits > 0) {
                 std::lock_guard<std::mutex> lock(mu);
                 memo.push_back({k, c->plan});
@@ -233,7 +239,7 @@ lf_status make_plan(lf_cache* c) {
     } else {
         if (!lf::simt_supported(G, g.head_dim))
             return fail(LF_ERR_UNSUPPORTED, "CUDA-core kernel not built for G=%d d=%d", G, g.head_dim);
-        c->plan = lf::simt_plan(plan_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
+        c->plan = lf::simt_plan(shard_units, G, g.head_dim, g.budget, g.split_tokens, c->num_sms);
         c->launch_clusters = 0;
     }
     if (c->plan.splits < 1 || c->plan.splits > 16)

@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _cases():
     out = []
-    for S in (1, 2, 4, 8, 16):
+    for S in (1, 2, 3, 4, 5, 6, 8, 16):
         for k in (1, 2):
             for solo in ((False,) if S == 1 else (False, True)):
                 for lat in ((False,) if S == 1 else (False, True)):
@@ -43,7 +43,7 @@ def test_plan_family_lockstep(cuda_lib, S, k, solo, lat):
     N = S * chunk - (37 if S > 1 else 0)
     Hq, Hkv = (32, 8) if (S + k) % 2 == 0 else (28, 4)
     kw = dict(split_tokens=chunk, ctas_per_sm=k, solo=solo, latency_variant=lat)
-    probe = Cache(64, Hq, Hkv, 128, N, **kw)
+    probe = Cache(1024 // Hkv, Hq, Hkv, 128, N, **kw)   # 1024 units: enough for a solo round
     C = probe.plan()["clusters"]
     probe.close()
     if solo:   # one round of whole units on every CTA plus a split tail of 37 units
@@ -62,18 +62,18 @@ def test_plan_family_lockstep(cuda_lib, S, k, solo, lat):
     assert st.evictions == 2 * B * Hkv and st.max_out_err < 1e-4, (plan, st)
 
 
-def _shard_run(wl, P, steps, seed, out_dtype, **kw):
+def _shard_run(wl, P, steps, seed, out_dtype, plan_shards=0, **kw):
     """Steps the whole batch on one cache and, on the same GPU, P shard caches of B/P sequences
-    each (plan_batch = B, seq_offset = r B/P), on the same inputs.  Returns per-step (out, slot,
-    scores) of both and the final caches."""
+    each (plan_batch = B, seq_offset = r B/P; both with the same plan_shards), on the same inputs.
+    Returns per-step (out, slot, scores) of both and the final caches."""
     from paper_2603_11504_b200 import Cache
     B, Bs = wl.B, wl.B // P
     K0, V0 = random_cache(B, wl.Hkv, wl.N, wl.d, seed=seed, device="cuda")
     syn = Synth(wl, seed=seed, device="cuda")
     inputs = [syn.step() for _ in range(steps)]
-    caches = [Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, **kw)]
-    caches += [Cache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, plan_batch=B, seq_offset=r * Bs, **kw)
-               for r in range(P)]
+    caches = [Cache(B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, plan_shards=plan_shards, **kw)]
+    caches += [Cache(Bs, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, plan_batch=B, seq_offset=r * Bs,
+                     plan_shards=plan_shards, **kw) for r in range(P)]
     rows = [slice(0, B)] + [slice(r * Bs, (r + 1) * Bs) for r in range(P)]
     for c, sl in zip(caches, rows):
         K, V, nv = c.views()
@@ -98,23 +98,26 @@ def _shard_run(wl, P, steps, seed, out_dtype, **kw):
     return res, views, plans
 
 
-SHARD_CASES = [  # (tag, B, Hq, Hkv, N, P, out_dtype)
-    ("q3", 64, 32, 8, 4096, 2, "bf16"),     # split S=2 with solo rounds: solo/split boundary inside a shard
-    ("q3", 64, 32, 8, 4096, 8, "f32"),
-    ("small", 8, 32, 8, 2048, 4, "f32"),    # machine-leaving grid: latency variant
-    ("g7", 16, 28, 4, 1024, 8, "bf16"),     # G = 7
-    ("r", 256, 32, 8, 8192, 8, "bf16"),     # configs[3] at 8 GPUs, the bench's strong-scaling shard
+SHARD_CASES = [  # (tag, B, Hq, Hkv, N, P, out_dtype, plan_shards)
+    ("q3", 64, 32, 8, 4096, 2, "bf16", 0),     # plan of the whole batch: solo/split boundary inside a shard
+    ("q3", 64, 32, 8, 4096, 8, "f32", 0),
+    ("q3", 64, 32, 8, 4096, 8, "bf16", 8),     # plan chosen for one of 8 shards (no solo rounds)
+    ("small", 8, 32, 8, 2048, 4, "f32", 4),    # machine-leaving grid: latency variant
+    ("g7", 16, 28, 4, 1024, 8, "bf16", 0),     # G = 7
+    ("r", 256, 32, 8, 8192, 8, "bf16", 8),     # configs[3] at 8 GPUs: bench.py's strong-scaling shards
+    ("r", 256, 32, 8, 8192, 2, "bf16", 2),
 ]
 
 
-@pytest.mark.parametrize("case", SHARD_CASES, ids=lambda c: f"{c[0]}_B{c[1]}_N{c[4]}_P{c[5]}_{c[6]}")
+@pytest.mark.parametrize("case", SHARD_CASES, ids=lambda c: f"{c[0]}_B{c[1]}_N{c[4]}_P{c[5]}_{c[6]}_ps{c[7]}")
 def test_sharded_equals_one_gpu(cuda_lib, case):
     """P logical shards, run one after another on one GPU with the plan of the global
-    batch (what bench.py's ranks do under --scaling strong), give out, scores and slots BIT-IDENTICAL
-    to the one-GPU run of the whole batch, step after step, and identical caches."""
-    tag, B, Hq, Hkv, N, P, out_dtype = case
+    problem (plan_batch, seq_offset, plan_shards: what bench.py's ranks do under --scaling strong),
+    give out, scores and slots BIT-IDENTICAL to a one-GPU cache of the whole batch with the same
+    plan_shards, step after step, and identical caches."""
+    tag, B, Hq, Hkv, N, P, out_dtype, ps = case
     wl = Workload(tag, B, Hq, Hkv, 128, N, 0, 4)
-    res, views, plans = _shard_run(wl, P, wl.steps, seed=7, out_dtype=out_dtype)
+    res, views, plans = _shard_run(wl, P, wl.steps, seed=7, out_dtype=out_dtype, plan_shards=ps)
     assert plans[0]["splits"] == plans[1]["splits"] and plans[0]["split_tokens"] == plans[1]["split_tokens"]
     for t, (full, shard) in enumerate(res):
         for a, b, name in zip(full, shard, ("out", "slot", "scores")):
@@ -137,6 +140,11 @@ def test_shard_plan_arguments(cuda_lib):
     assert e.value.status == 1
     c = Cache(4, 8, 2, 128, 256, plan_batch=8, seq_offset=4)
     assert c.plan()["kernel"] == "tcgen05"
+    with pytest.raises(LFError) as e:   # plan_shards plans have no whole-unit rounds
+        Cache(4, 8, 2, 128, 256, plan_shards=2, solo=True)
+    assert e.value.status == 1
+    c = Cache(64, 32, 8, 128, 4096, plan_batch=256, seq_offset=64, plan_shards=4)
+    assert c.plan()["solo_rounds"] == 0
 
 
 LIVENESS = [  # (budgets, batches, ctas_per_sm, split_tokens, solo)
