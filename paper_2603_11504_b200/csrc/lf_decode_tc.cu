@@ -127,11 +127,29 @@ static_assert(NBARS <= 48, "barrier slots");
         if ((t_) < 32) LF_EVENT((ui_) + (row_), (t_)); \
     } while (0)
 
-__device__ __forceinline__ float habs_sum8(const uint4& w) {
-    return (fabsf(__uint_as_float(w.x << 16)) + fabsf(__uint_as_float(w.x & 0xffff0000u))) +
-           (fabsf(__uint_as_float(w.y << 16)) + fabsf(__uint_as_float(w.y & 0xffff0000u))) +
-           (fabsf(__uint_as_float(w.z << 16)) + fabsf(__uint_as_float(w.z & 0xffff0000u))) +
-           (fabsf(__uint_as_float(w.w << 16)) + fabsf(__uint_as_float(w.w & 0xffff0000u)));
+// acc + sum of |v| over the 8 bf16 of w, in fp32: one LOP3 clears both sign bits of a pair and each
+// element is added straight from its register half by the sm_100 mixed-precision add (FHADD.BF16,
+// PTX add.rn.f32.bf16): 12 instructions per 8 values instead of 16 with explicit unpacking.
+__device__ __forceinline__ float habs_acc8(const uint4& w, float acc) {
+    const uint32_t p[4] = {w.x & 0x7fff7fffu, w.y & 0x7fff7fffu, w.z & 0x7fff7fffu, w.w & 0x7fff7fffu};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        asm("{\n\t.reg .b16 lo, hi;\n\tmov.b32 {lo, hi}, %1;\n\t"
+            "add.rn.f32.bf16 %0, lo, %0;\n\tadd.rn.f32.bf16 %0, hi, %0;\n\t}"
+            : "+f"(acc)
+            : "r"(p[i]));
+    return acc;
+}
+// lambda_j = ||v_j||_1 of one token row of a landed V tile (both 64-column SW128 boxes), two
+// independent accumulators
+__device__ __forceinline__ float row_l1(const unsigned char* Vt, int row) {
+    float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        a0 = habs_acc8(*(const uint4*)(Vt + row * 128 + ((k ^ (row & 7)) << 4)), a0);
+        a1 = habs_acc8(*(const uint4*)(Vt + kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)), a1);
+    }
+    return a0 + a1;
 }
 
 struct UnitInfo {
@@ -603,11 +621,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 float lam = 0.f;
                 if (row < nv) {
-#pragma unroll
-                    for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)));
+                    lam = row_l1(Vt, row);
                 } else {
 #pragma unroll
                     for (int bb = 0; bb < 2; ++bb)
@@ -695,13 +709,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 }
                 // lambda_j from the landed tile, before PREADY: after the PV MMA the stage is refilled
                 float lam = 0.f;
-                if (valid) {
-#pragma unroll
-                    for (int bb = 0; bb < 2; ++bb)
-#pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            lam += habs_sum8(*(const uint4*)(Vt + bb * kBoxBytes + row * 128 + ((k ^ (row & 7)) << 4)));
-                }
+#ifdef LF_ATTR_NO_LAMBDA   // attribution builds only (results wrong): no lambda pass over the V tile
+                lam = valid ? 1.f : 0.f;
+#else
+                if (valid) lam = row_l1(Vt, row);
+#endif
                 Ls[tok] = lam;
                 }
                 ptx::fence_proxy_async_smem();
