@@ -688,8 +688,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     if (g < G) {
                         const float pv = valid ? ptx::ex2_approx(__uint_as_float(r[g]) * sl2 - m[g]) : 0.f;
                         z[g] += pv;
-                        const uint16_t hi = f32_to_bf16_rne(pv);
-                        const uint16_t lo = f32_to_bf16_rne(pv - bf16_to_f32(hi));
+                        const uint16_t hi = ptx::cvt_bf16_rn(pv);   // hardware RNE (pv is finite)
+                        const uint16_t lo = ptx::cvt_bf16_rn(pv - bf16_to_f32(hi));
                         *(uint16_t*)(P + g * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = hi;
                         *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
                     }

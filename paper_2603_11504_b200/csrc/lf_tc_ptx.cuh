@@ -204,6 +204,13 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// fp32 -> bf16 round-to-nearest-even in one instruction (F2FP); identical to the software RNE for
+// finite inputs (NaN encodings differ)
+__device__ __forceinline__ uint16_t cvt_bf16_rn(float x) {
+    uint16_t r;
+    asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(r) : "f"(x));
+    return r;
+}
 // fast SFU transcendentals (rel. error ~2^-22; denormals flushed)
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
