@@ -193,10 +193,13 @@ __device__ __forceinline__ UnitInfo item_base(const StepParams& p, int cid, int 
     return x;
 }
 // ... plus the unit's fill state n (after the PDL wait: the previous step may have appended)
-__device__ __forceinline__ void set_fill(UnitInfo& x, int n) {
+// one_tile: a latency-variant split item whose CTA share is a single 128-token tile is always
+// processed as ONE tile, even when none of its rows is valid yet (fill phase): its K and V tiles can
+// then be requested before the fill state arrives (P = 0 and zeroed V rows make an empty tile exact)
+__device__ __forceinline__ void set_fill(UnitInfo& x, int n, bool one_tile = false) {
     x.n = n;
     x.nv = max(0, min(x.c1, x.n) - x.c0);
-    x.ntiles = (x.nv + 127) / 128;
+    x.ntiles = one_tile ? 1 : (x.nv + 127) / 128;
 }
 // tokens one CTA may hold for a unit (TMEM regions, lambda buffer)
 __host__ __device__ inline int hold_tokens(int N, int chunk, bool solo) {
@@ -328,14 +331,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 uint4 qv[4];
 #pragma unroll
                 for (int k = 0; k < 4; ++k) qv[k] = lane + 32 * k < G * 16 ? __ldg(qg + lane + 32 * k) : make_uint4(0, 0, 0, 0);
-                set_fill(x, __ldcg(p.n_valid + u));
-                if (lane == 0) {   // publish n: the only read of n_valid in the CTA
-                    nsm[i & 7] = x.n;
-                    ptx::mbar_arrive(BAR(NRDY + (i & 7)));
-                }
-                if (lane == 0 && i == 0) LF_EVENT(0, 22);
-                // the first ring stages go out before Q is staged (they do not depend on it)
-                const int pre = min(2 * x.ntiles, ST);
+                const int nval = __ldcg(p.n_valid + u);
+                const bool one = x.split && p.chunk == 128;
                 auto issue = [&](int i) {
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
@@ -348,7 +345,22 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
                     ++it;
                 };
-                if (lane == 0)
+                if (one) {   // K and V tile 0 go out before the fill state returns (one round trip less)
+                    x.ntiles = 1;
+                    if (lane == 0) {
+                        issue(0);
+                        issue(1);
+                    }
+                }
+                set_fill(x, nval, one);
+                if (lane == 0) {   // publish n: the only read of n_valid in the CTA
+                    nsm[i & 7] = x.n;
+                    ptx::mbar_arrive(BAR(NRDY + (i & 7)));
+                }
+                if (lane == 0 && i == 0) LF_EVENT(0, 22);
+                // the first ring stages go out before Q is staged (they do not depend on it)
+                const int pre = one ? 2 : min(2 * x.ntiles, ST);
+                if (lane == 0 && !one)
                     for (int i = 0; i < pre; ++i) issue(i);
                 ptx::mbar_wait(BAR(QFREE + qb), ((qi >> 1) & 1u) ^ 1u);
                 if (lane == 0 && i == 0) LF_EVENT(0, 24);
@@ -425,7 +437,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
                 ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
-                set_fill(x, nsm[i & 7]);
+                set_fill(x, nsm[i & 7], kLat && x.split && p.chunk == 128);
                 const uint32_t par = ui & 1u;
                 LF_PROG(1, ((unsigned long long)i << 32) | it);
                 ptx::mbar_wait(BAR(QFULL + par), (ui >> 1) & 1u);
@@ -565,7 +577,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     xk = __ldg((const uint4*)(p.k_new + (size_t)u * 128) + xch);
                 }
                 ptx::mbar_wait(BAR(NRDY + (i & 7)), (uint32_t)(i >> 3) & 1u);
-                set_fill(x, nsm[i & 7]);
+                set_fill(x, nsm[i & 7], x.split && p.chunk == 128);
                 if (sidx == 0 && i == 0) LF_EVENT(0, 21);
                 if (warp == 2 + 4 * kNG - 1) kvn[lane] = kvw;
                 if (sidx < 128) {
