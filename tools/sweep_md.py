@@ -8,9 +8,10 @@ Bs = sorted({r["B"] for r in rows})
 d = {(r["B"], r["N"]): r for r in rows}
 print(f"# {sys.argv[2] if len(sys.argv) > 2 else 'Budget sweep'}\n")
 print("latency per decode step (us) / fraction of the measured HBM copy peak; 32/8 GQA, d=128, full cache, "
-      "bf16 out, CUDA graph of back-to-back steps. Unmarked: cache > 512 MB (larger than L2). "
-      "`L`: cache < 512 MB, L = ceil(4 x L2 / cache) layer caches cycled in the graph so each step's cache is cold "
-      "in L2 (SURVEY D.4); the step time is per layer call.\n")
+      "bf16 out, CUDA graph of back-to-back steps. Unmarked: cache >= 1 GB (far larger than the 126 MB L2). "
+      "`L`: cache < 1 GB, L = ceil(8 x L2 / cache) layer caches cycled in the graph so each step's cache is cold "
+      "in L2 (SURVEY D.4); the step time is per layer call. `*`: every step timed alone after an untimed 512 MB "
+      "read that evicts L2.\n")
 print("| B \\ N | " + " | ".join(map(str, Ns)) + " |")
 print("|---" * (len(Ns) + 1) + "|")
 for B in Bs:
