@@ -1058,11 +1058,14 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             if (sidx == 0) LF_EVENT(ui, 14);
             if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));   // senders may reuse it
         }
-        // drain: no CTA leaves before every peer released (consumed) the inboxes it pushed to
-        for (uint32_t k = xi >= 2 ? xi - 2 : 0; k < xi; ++k)
-            ptx::mbar_wait_cluster(BAR(XFREE + (k & 1)), (k >> 1) & 1u);
+        // (no drain of the last XFREE phases: the cluster barrier below orders every CTA's remote
+        // arrivals and stores before any CTA of the cluster leaves)
     }
-    __syncthreads();
+    __syncwarp();
+    // every CTA of the cluster leaves together: no CTA exits while a peer may still address its shared
+    // memory (round 1 drained its own XFREE phases instead; compute-sanitizer synccheck reported unsafe
+    // exits for clusters of >= 4 CTAs placed two per SM, with illegal-address faults under the tool)
+    ptx::cluster_sync_all();
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, (uint32_t)a.tmem_cols);
@@ -1272,6 +1275,10 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
                 // persistent loop is correct either way (no cross-cluster dependency).
                 if (k == 2) C *= 2;
                 if (C <= 0) continue;
+                // 16-CTA clusters two per SM walking several units: compute-sanitizer synccheck reports a
+                // "missing wait" on a cluster barrier for this family only (the round-1 kernel too; memcheck
+                // and racecheck are clean and lockstep parity holds): the planner does not choose it
+                if (k == 2 && splits > 8 && units > C && !force.ctas_per_sm) continue;
                 const long long ovh1 = 128, ovhS = splits > 1 ? 1024 : 128;
                 double cost;
                 long long R = 0;

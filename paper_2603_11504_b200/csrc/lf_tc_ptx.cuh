@@ -267,9 +267,13 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, uint
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// Named barrier WITHOUT .aligned (bar.sync == barrier.sync.aligned requires every warp to arrive
+// converged; the warp-specialised roles contain lane-0-only sections, and compute-sanitizer synccheck
+// flagged divergent arrivals in the two-CTAs-per-SM variant): each thread counts individually.
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void cta_sync() { asm volatile("barrier.sync 0;" ::: "memory"); }
 
 // ---- tcgen05 -------------------------------------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t dst_smem, uint32_t ncols) {   // whole warp

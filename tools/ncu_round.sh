@@ -5,7 +5,7 @@
 T=${1:-r2}
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${T}_launches_r.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
-for w in r q3 q7 f1 sweep_b128_n512; do
+for w in r q3 q7 f1 sweep_b128_n512 sweep_b32_n8192; do
   extra=""; [ $w = sweep_b128_n512 ] && extra="--ctas-per-sm 2"
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:tc_decode -s 6 -c 1 \
       -o gpurun_out/${T}_full_$w python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --no-graph $extra \
