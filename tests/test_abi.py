@@ -35,7 +35,23 @@ def test_status_strings():
         assert lib.lf_status_string(code).decode() == name
 
 
+def test_config_struct_matches_header():
+    """binding.CacheConfig mirrors lf_cache_config field by field (names, order, 4-byte types)."""
+    src = open(os.path.join(ROOT, "include", "longflow.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} lf_cache_config;", src, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"\b(int32_t|float)\s+(\w+)\s*;", body)
+    assert [n for _, n in fields] == [n for n, _ in binding.CacheConfig._fields_]
+    assert ctypes.sizeof(binding.CacheConfig) == 4 * len(fields)
+
+
 @pytest.mark.parametrize("kw,status", [
+    (dict(plan_batch=1), 1),              # the global batch smaller than this cache
+    (dict(seq_offset=2), 1),              # seq_offset without plan_batch
+    (dict(plan_batch=4, seq_offset=3), 1),   # shard past the global batch
+    (dict(plan_shards=-1), 1),
+    (dict(plan_shards=2, solo=True), 1),  # plan_shards plans have no whole-unit rounds
+    (dict(ctas_per_sm=3), 1),
     (dict(budget=1), 1),                  # S:125 budget < 2
     (dict(num_q_heads=6, num_kv_heads=4), 1),
     (dict(head_dim=96), 2),               # not built

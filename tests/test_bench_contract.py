@@ -46,7 +46,7 @@ def test_warmup_floor():
 
 
 def test_l2_methods():
-    """Caches larger than L2 run back to back; L2-resident ones cycle >= 4 x L2 of layer caches; only
+    """Caches larger than L2 run back to back; L2-resident ones cycle >= 8 x L2 of layer caches; only
     caches too small for <= 256 layers fall back to per-step timing after an L2 flush."""
     big = bench.cache_bytes_per_gpu(CONFIGS["r"], 256)
     assert big > bench.FLUSH_BELOW and bench.layers_for(big) == 1

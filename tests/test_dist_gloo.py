@@ -1,7 +1,7 @@
 """Multi-process (gloo, world size 2, CPU) checks of the sequence-sharded path's host logic:
 shard arithmetic, sharding-stable input generation, and that the per-rank results gathered in rank
 order equal the single-process full-batch results (the oracle stands in for the GPU step here; the GPU
-equivalence itself follows because units never interact)."""
+kernel's own shard bit-identity is tests/test_gpu_plans.py::test_sharded_equals_one_gpu)."""
 import os
 import socket
 
