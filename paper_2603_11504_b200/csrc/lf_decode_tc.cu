@@ -289,9 +289,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         if (x.valid) {
             const int u = x.u;
             ptx::bulk_prefetch_l2(p.n_valid + (u & ~3), 16);
-            ptx::bulk_prefetch_l2(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128, (uint32_t)G * 256);
-            ptx::bulk_prefetch_l2(p.k_new + (size_t)u * 128, 256);
-            ptx::bulk_prefetch_l2(p.v_new + (size_t)u * 128, 256);
+            if (!p.host_io) {
+                ptx::bulk_prefetch_l2(p.q + ((size_t)x.b * p.Hq + (size_t)x.h * G) * 128, (uint32_t)G * 256);
+                ptx::bulk_prefetch_l2(p.k_new + (size_t)u * 128, 256);
+                ptx::bulk_prefetch_l2(p.v_new + (size_t)u * 128, 256);
+            }
             const int nt = min((x.c1 - x.c0 + 127) / 128, 4);
             for (int t = 0; t < nt; ++t) {
                 const int row = u * N + x.c0 + t * 128;

@@ -145,7 +145,8 @@ struct lf_cache {
     std::vector<unsigned char> needs_pend;   // deferred modes: sequence full after prefill, no victim yet
     lf::TcMaps maps;
     unsigned long long* trace;
-    char* host_stage;      // pinned staging for small lf_decode_step_host calls (one H2D + one D2H)
+    char* host_stage;      // mapped pinned staging for small lf_decode_step_host calls (zero-copy)
+    char* host_stage_dev;  // its device-side address
 };
 
 namespace {
@@ -323,10 +324,14 @@ lf_status lf_cache_create(const lf_cache_config* cfg, int device, void* device_b
     }
     c->slab_bytes = c->L.total;
     c->host_stage = nullptr;
+    c->host_stage_dev = nullptr;
     if (stage_in_bytes(c->L, c->cfg) + stage_out_bytes(c->L, c->cfg) <= kPackLimit) {
         if (cudaHostAlloc((void**)&c->host_stage, stage_in_bytes(c->L, c->cfg) + stage_out_bytes(c->L, c->cfg),
-                          cudaHostAllocDefault) != cudaSuccess) {
+                          cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess ||
+            cudaHostGetDevicePointer((void**)&c->host_stage_dev, c->host_stage, 0) != cudaSuccess) {
+            if (c->host_stage) cudaFreeHost(c->host_stage);
             c->host_stage = nullptr;   // optional: fall back to one copy per tensor
+            c->host_stage_dev = nullptr;
             cudaGetLastError();
         }
     }
@@ -540,8 +545,16 @@ lf_status lf_diagnose_step(lf_cache* c, const void* q, const void* k_new, const 
     return LF_OK;
 }
 
+static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
+                             int32_t* slot, float* scores, void* stream, int host_io);
+
 lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
                          int32_t* slot, float* scores, void* stream) {
+    return decode_impl(c, q, k_new, v_new, out, slot, scores, stream, 0);
+}
+
+static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
+                             int32_t* slot, float* scores, void* stream, int host_io) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
     if (!q || !k_new || !v_new || !out || !slot)
         return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new, out and slot must be non-NULL");
@@ -585,6 +598,7 @@ lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const vo
     p.splits = c->plan.splits;
     p.chunk = c->plan.chunk;
     p.solo_units = c->solo_units;
+    p.host_io = host_io;
     p.hold = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_hold(c->plan, g.budget) : 0;
     lf::Plan lp = c->plan;
     lp.clusters = c->launch_clusters;
@@ -613,41 +627,44 @@ lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new
     size_t kb = (size_t)g.batch * g.num_kv_heads * g.head_dim * 2;
     size_t ob = (size_t)g.batch * g.num_q_heads * g.head_dim * (g.out_dtype == LF_DTYPE_F32 ? 4 : 2);
     size_t sb = (size_t)g.batch * g.num_kv_heads * 4;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(c->device);
-    cudaError_t e;
     char* hs = c->host_stage;
-    const size_t in_b = stage_in_bytes(c->L, g);
-    if (hs) {   // small step: pack the three inputs, one H2D copy
+    if (hs) {
+        // small step, zero-copy: the inputs are packed into the mapped pinned staging buffer, the kernel
+        // reads them and writes out + slot there directly over the host link, one stream sync
         memcpy(hs, q_host, qb);
         memcpy(hs + (c->L.sk_off - c->L.sq_off), k_new_host, kb);
         memcpy(hs + (c->L.sv_off - c->L.sq_off), v_new_host, kb);
-        e = cudaMemcpyAsync(base + c->L.sq_off, hs, in_b, cudaMemcpyHostToDevice, st);
-    } else {
-        e = cudaMemcpyAsync(base + c->L.sq_off, q_host, qb, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sk_off, k_new_host, kb, cudaMemcpyHostToDevice, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sv_off, v_new_host, kb, cudaMemcpyHostToDevice, st);
+        char* hd = c->host_stage_dev;
+        const size_t in_b = stage_in_bytes(c->L, g);
+        const size_t so = in_b, ss = in_b + (c->L.ss_off - c->L.so_off);
+        lf_status s = decode_impl(c, hd, hd + (c->L.sk_off - c->L.sq_off), hd + (c->L.sv_off - c->L.sq_off),
+                                  hd + so, (int32_t*)(hd + ss), nullptr, stream, 1);
+        if (s) return s;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(c->device);
+        const cudaError_t e = cudaStreamSynchronize(st);
+        cudaSetDevice(prev);
+        if (e != cudaSuccess) return cuda_fail(e, "host step");
+        memcpy(out_host, hs + so, ob);
+        memcpy(slot_host, hs + ss, sb);
+        return LF_OK;
     }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaError_t e = cudaMemcpyAsync(base + c->L.sq_off, q_host, qb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sk_off, k_new_host, kb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(base + c->L.sv_off, v_new_host, kb, cudaMemcpyHostToDevice, st);
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "h2d");
     lf_status s = lf_decode_step(c, base + c->L.sq_off, base + c->L.sk_off, base + c->L.sv_off,
                                  base + c->L.so_off, (int32_t*)(base + c->L.ss_off), nullptr, stream);
     if (s) return s;
     cudaSetDevice(c->device);
-    if (hs) {   // one D2H copy of out + slot, then unpack
-        char* ho = hs + in_b;
-        e = cudaMemcpyAsync(ho, base + c->L.so_off, stage_out_bytes(c->L, g), cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-        if (e == cudaSuccess) {
-            memcpy(out_host, ho, ob);
-            memcpy(slot_host, ho + (c->L.ss_off - c->L.so_off), sb);
-        }
-    } else {
-        e = cudaMemcpyAsync(out_host, base + c->L.so_off, ob, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(slot_host, base + c->L.ss_off, sb, cudaMemcpyDeviceToHost, st);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    }
+    e = cudaMemcpyAsync(out_host, base + c->L.so_off, ob, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(slot_host, base + c->L.ss_off, sb, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_fail(e, "d2h");
     return LF_OK;
