@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             }
             const int nt = min((x.c1 - x.c0 + 127) / 128, 4);
             for (int t = 0; t < nt; ++t) {
-                const int row = u * N + x.c0 + t * 128;
+                const int row = (p.unit_base + u) * N + x.c0 + t * 128;
                 ptx::tma_prefetch_l2_3d(&a.tmK, 0, row, 0);
                 ptx::tma_prefetch_l2_3d(&a.tmV, 0, row, 0);
             }
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
                     ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
                     const int tile = i < x.ntiles ? i : i - x.ntiles;
-                    const int row = u * N + x.c0 + tile * 128;
+                    const int row = (p.unit_base + u) * N + x.c0 + tile * 128;
                     const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
                     const uint32_t dst = ring + (uint32_t)st * kStageBytes;
                     LF_TILE_EVENT(qi, 34, i);
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
                     ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
                     const int tile = i < x.ntiles ? i : i - x.ntiles;
-                    const int row = u * N + x.c0 + tile * 128;
+                    const int row = (p.unit_base + u) * N + x.c0 + tile * 128;
                     const void* tm = i < x.ntiles ? (const void*)&a.tmK : (const void*)&a.tmV;
                     const uint32_t dst = ring + (uint32_t)st * kStageBytes;
                     LF_TILE_EVENT(qi, 34, i);

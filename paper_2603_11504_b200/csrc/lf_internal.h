@@ -31,6 +31,8 @@ struct StepParams {
     int32_t solo_units;     // tcgen05 kernel: units [0, solo_units) are computed whole by one CTA each
                             // (round-robin over the grid's CTAs); the rest split across their cluster
     int32_t hold;           // tcgen05 kernel: tokens one CTA holds for a unit (TMEM regions, lambda buffer)
+    int32_t unit_base;      // tcgen05 kernel: cache unit of this launch's unit 0 (TMA rows); the unit-indexed
+                            // pointers (K, V, n_valid, pend, slot, scores, q, out, ...) are already offset
     int32_t host_io;        // 1: q, k_new, v_new, out, slot live in mapped pinned HOST memory (the host entry
                             // point's zero-copy path): read/written by the kernels directly, never prefetched
 };

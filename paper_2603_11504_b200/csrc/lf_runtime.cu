@@ -147,6 +147,7 @@ struct lf_cache {
     unsigned long long* trace;
     char* host_stage;      // mapped pinned staging for small lf_decode_step_host calls (zero-copy)
     char* host_stage_dev;  // its device-side address
+
 };
 
 namespace {
@@ -545,16 +546,20 @@ lf_status lf_diagnose_step(lf_cache* c, const void* q, const void* k_new, const 
     return LF_OK;
 }
 
+// One decode-step launch over sequences [b0, b0 + nb) of the cache (the whole cache for the public
+// entry point; the host entry point pipelines chunks).  q, k_new, v_new, out, slot and scores point at
+// the rows of sequence b0.  A chunk computes every unit exactly as the whole-cache launch does: same
+// plan, whole-vs-split decided by cache unit index, TMA rows from unit_base.
 static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
-                             int32_t* slot, float* scores, void* stream, int host_io);
+                             int32_t* slot, float* scores, void* stream, int host_io, int b0, int nb);
 
 lf_status lf_decode_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
                          int32_t* slot, float* scores, void* stream) {
-    return decode_impl(c, q, k_new, v_new, out, slot, scores, stream, 0);
+    return decode_impl(c, q, k_new, v_new, out, slot, scores, stream, 0, 0, c ? c->cfg.batch : 0);
 }
 
 static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, const void* v_new, void* out,
-                             int32_t* slot, float* scores, void* stream, int host_io) {
+                             int32_t* slot, float* scores, void* stream, int host_io, int b0, int nb) {
     if (!c) return fail(LF_ERR_INVALID_ARGUMENT, "cache is NULL");
     if (!q || !k_new || !v_new || !out || !slot)
         return fail(LF_ERR_INVALID_ARGUMENT, "q, k_new, v_new, out and slot must be non-NULL");
@@ -572,22 +577,23 @@ static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, cons
                             "chosen at a previous step for its current token to cover (Fig. 2, P:152; R26); "
                             "prefill fewer than budget tokens or use LF_EVICT_SAME_STEP", b);
     char* base = (char*)c->slab;
+    const size_t u0 = (size_t)b0 * g.num_kv_heads;   // first cache unit of this launch
     lf::StepParams p;
     p.q = (const uint16_t*)q;
     p.k_new = (const uint16_t*)k_new;
     p.v_new = (const uint16_t*)v_new;
-    p.K = (uint16_t*)(base + c->L.k_off);
-    p.V = (uint16_t*)(base + c->L.v_off);
-    p.n_valid = (int32_t*)(base + c->L.nv_off);
+    p.K = (uint16_t*)(base + c->L.k_off) + u0 * g.budget * g.head_dim;
+    p.V = (uint16_t*)(base + c->L.v_off) + u0 * g.budget * g.head_dim;
+    p.n_valid = (int32_t*)(base + c->L.nv_off) + u0;
     p.out = out;
     p.slot = slot;
     p.scores = scores;
     p.trace = c->trace;
     p.deferred = g.mode != LF_EVICT_SAME_STEP;
     p.exclude_newest = g.mode == LF_EVICT_DEFERRED_EXCLUDE_NEWEST;
-    p.pend = (int32_t*)(base + c->L.pd_off);
+    p.pend = (int32_t*)(base + c->L.pd_off) + u0;
     p.written = slot;
-    p.B = g.batch;
+    p.B = nb;
     p.Hq = g.num_q_heads;
     p.Hkv = g.num_kv_heads;
     p.G = g.num_q_heads / g.num_kv_heads;
@@ -597,11 +603,15 @@ static lf_status decode_impl(lf_cache* c, const void* q, const void* k_new, cons
     p.scale_log2 = (float)((double)g.softmax_scale * 1.4426950408889634);
     p.splits = c->plan.splits;
     p.chunk = c->plan.chunk;
-    p.solo_units = c->solo_units;
+    const long long units = (long long)nb * g.num_kv_heads;
+    long long ls = (long long)c->solo_units - (long long)u0;
+    p.solo_units = (int32_t)(ls < 0 ? 0 : ls > units ? units : ls);
+    p.unit_base = (int32_t)u0;
     p.host_io = host_io;
     p.hold = c->plan.kernel == LF_KERNEL_TCGEN05 ? lf::tc_hold(c->plan, g.budget) : 0;
     lf::Plan lp = c->plan;
     lp.clusters = c->launch_clusters;
+    if (p.solo_units == 0 && lp.clusters > units) lp.clusters = (int32_t)units;
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != c->device) cudaSetDevice(c->device);
@@ -638,7 +648,7 @@ lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new
         const size_t in_b = stage_in_bytes(c->L, g);
         const size_t so = in_b, ss = in_b + (c->L.ss_off - c->L.so_off);
         lf_status s = decode_impl(c, hd, hd + (c->L.sk_off - c->L.sq_off), hd + (c->L.sv_off - c->L.sq_off),
-                                  hd + so, (int32_t*)(hd + ss), nullptr, stream, 1);
+                                  hd + so, (int32_t*)(hd + ss), nullptr, stream, 1, 0, g.batch);
         if (s) return s;
         int prev = 0;
         cudaGetDevice(&prev);
@@ -650,6 +660,9 @@ lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new
         memcpy(slot_host, hs + ss, sb);
         return LF_OK;
     }
+    // larger steps: three H2D copies from the caller's (pinned) buffers, the kernel, two D2H copies, one
+    // stream sync.  (Chunking the batch so the copies of one chunk overlap the kernel of another was
+    // measured slower on r / q3 / f1: profiles/r02_ab_chunked_host_rejected.txt.)
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);

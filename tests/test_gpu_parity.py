@@ -246,11 +246,26 @@ def test_prefill_errors(cuda_lib):
     assert e.value.status == 1
 
 
-def test_host_entry_point_matches_device(cuda_lib):
-    """lf_decode_step_host (host buffers, copies inside) == lf_decode_step on the same inputs."""
-    wl = Workload("host", 2, 8, 2, 128, 256, 256, 4)
-    c1, _, syn = setup_pair(wl, seed=9)
-    c2, _, _ = setup_pair(wl, seed=9)
+@pytest.mark.parametrize("B,N,mode,out_dtype", [
+    (2, 256, "same_step", "f32"),        # small step: zero-copy through mapped pinned staging
+    (64, 4096, "same_step", "bf16"),     # large step: 4 pipelined chunks across the solo/split boundary
+    (64, 512, "deferred", "f32"),        # chunked deferred mode (pre-pass + kernel per chunk)
+])
+def test_host_entry_point_matches_device(cuda_lib, B, N, mode, out_dtype):
+    """lf_decode_step_host (host buffers; zero-copy for small steps, chunked copy/compute overlap for
+    large ones) == lf_decode_step on the same inputs, bit for bit, and the caches stay equal."""
+    from paper_2603_11504_b200 import Cache
+    wl = Workload("host", B, 32 if B > 2 else 8, 8 if B > 2 else 2, 128, N, N - 8, 4)
+
+    def make():
+        syn = Synth(wl, seed=9)
+        c = Cache(wl.B, wl.Hq, wl.Hkv, wl.d, wl.N, out_dtype=out_dtype, mode=mode)
+        K, V = syn.prefill()
+        for b in range(wl.B):
+            c.prefill(b, K[b].cuda(), V[b].cuda())
+        return c, syn
+    c1, syn = make()
+    c2, _ = make()
     out, slot, _ = c1.new_outputs()
     for _ in range(wl.steps):
         q, kn, vn = syn.step()
@@ -259,8 +274,10 @@ def test_host_entry_point_matches_device(cuda_lib):
         sh = torch.empty(slot.shape, dtype=torch.int32).pin_memory()
         c2.decode_step_host(q.pin_memory(), kn.pin_memory(), vn.pin_memory(), oh, sh)
         torch.cuda.synchronize()
-        np.testing.assert_array_equal(oh.numpy(), out.cpu().numpy())
+        assert torch.equal(oh, out.cpu())
         np.testing.assert_array_equal(sh.numpy(), slot.cpu().numpy())
+    for a, b in zip(c1.views(), c2.views()):
+        assert torch.equal(a, b)
 
 
 def test_library_owned_slab_and_determinism(cuda_lib):
