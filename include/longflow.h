@@ -163,9 +163,11 @@ lf_status lf_diag_workspace_bytes(const lf_cache* c, size_t* bytes);
 lf_status lf_diagnose_step(lf_cache* c, const void* q, const void* k_new, const void* v_new, int32_t* islot,
                            float* fstat, void* workspace, void* stream);
 
-/* Same step with HOST buffers (the end-to-end entry point): copies q/k_new/v_new host ->
- * device (pinned host memory recommended), runs lf_decode_step on `stream`, copies out and
- * slot device -> host and synchronises `stream` before returning. Layouts as above. */
+/* Same step with HOST buffers (the end-to-end entry point), synchronous: small steps (<= 256 KB of
+ * I/O) are packed into the cache's mapped pinned staging buffer and the kernel reads the inputs and
+ * writes out/slot there directly (zero-copy); larger steps copy q/k_new/v_new host -> device (pinned
+ * host memory recommended), run lf_decode_step on `stream` and copy out and slot device -> host.
+ * `stream` is synchronised before returning. Layouts as above. */
 lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new_host,
                               const void* v_new_host, void* out_host, int32_t* slot_host,
                               void* stream);
@@ -195,8 +197,9 @@ lf_status lf_cache_pending(const lf_cache* c, int32_t** pend);
 /* Number of CUDA kernels lf_decode_step launches per call (for launch accounting). */
 int32_t lf_kernels_per_step(const lf_cache* c);
 
-/* Debug only: device buffer receiving per-CTA %globaltimer events from builds compiled with
- * -DLF_TRACE (ignored otherwise); NULL disables.  Layout: see DESIGN.md "Tracing". */
+/* Debug only: buffer receiving per-CTA %globaltimer events from builds compiled with -DLF_TRACE, or
+ * (mapped pinned host memory) the stuck-wait log and progress counters of -DLF_HANG_DIAG builds
+ * (tools/hang_diag.py); ignored by the product build; NULL disables.  Layout: DESIGN.md "Tracing". */
 lf_status lf_debug_set_trace(lf_cache* c, void* device_buf);
 
 const char* lf_status_string(lf_status s);
