@@ -637,6 +637,35 @@ lf_status lf_decode_step_host(lf_cache* c, const void* q_host, const void* k_new
     size_t kb = (size_t)g.batch * g.num_kv_heads * g.head_dim * 2;
     size_t ob = (size_t)g.batch * g.num_q_heads * g.head_dim * (g.out_dtype == LF_DTYPE_F32 ? 4 : 2);
     size_t sb = (size_t)g.batch * g.num_kv_heads * 4;
+    // Caller buffers in pinned, device-mapped host memory (e.g. torch pin_memory): the kernel reads the
+    // inputs and writes out/slot there directly over the host link, overlapped with its own K/V
+    // streaming -- no copy at all, one stream sync.
+    {
+        auto mapped = [](const void* h) -> void* {
+            cudaPointerAttributes a;
+            if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+            return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+        };
+        void* dq = mapped(q_host);
+        void* dk = dq ? mapped(k_new_host) : nullptr;
+        void* dv = dk ? mapped(v_new_host) : nullptr;
+        void* dout = dv ? mapped(out_host) : nullptr;
+        void* dslot = dout ? mapped(slot_host) : nullptr;
+        if (dslot) {
+            lf_status s = decode_impl(c, dq, dk, dv, dout, (int32_t*)dslot, nullptr, stream, 1, 0, g.batch);
+            if (s) return s;
+            int prev = 0;
+            cudaGetDevice(&prev);
+            cudaSetDevice(c->device);
+            const cudaError_t e = cudaStreamSynchronize(st);
+            cudaSetDevice(prev);
+            if (e != cudaSuccess) return cuda_fail(e, "host step");
+            return LF_OK;
+        }
+    }
     char* hs = c->host_stage;
     if (hs) {
         // small step, zero-copy: the inputs are packed into the mapped pinned staging buffer, the kernel

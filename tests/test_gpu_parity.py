@@ -246,14 +246,16 @@ def test_prefill_errors(cuda_lib):
     assert e.value.status == 1
 
 
+@pytest.mark.parametrize("pinned", [True, False], ids=["pinned", "pageable"])
 @pytest.mark.parametrize("B,N,mode,out_dtype", [
-    (2, 256, "same_step", "f32"),        # small step: zero-copy through mapped pinned staging
-    (64, 4096, "same_step", "bf16"),     # large step: 4 pipelined chunks across the solo/split boundary
-    (64, 512, "deferred", "f32"),        # chunked deferred mode (pre-pass + kernel per chunk)
+    (2, 256, "same_step", "f32"),        # small step (pageable: zero-copy through the mapped staging)
+    (64, 4096, "same_step", "bf16"),     # large step (pageable: H2D, kernel, D2H) across solo/split units
+    (64, 512, "deferred", "f32"),        # deferred mode (pre-pass + kernel)
 ])
-def test_host_entry_point_matches_device(cuda_lib, B, N, mode, out_dtype):
-    """lf_decode_step_host (host buffers; zero-copy for small steps, chunked copy/compute overlap for
-    large ones) == lf_decode_step on the same inputs, bit for bit, and the caches stay equal."""
+def test_host_entry_point_matches_device(cuda_lib, B, N, mode, out_dtype, pinned):
+    """lf_decode_step_host (host buffers: pinned caller buffers are read and written by the kernel
+    directly, pageable ones go through the staging) == lf_decode_step on the same inputs, bit for
+    bit, and the caches stay equal."""
     from paper_2603_11504_b200 import Cache
     wl = Workload("host", B, 32 if B > 2 else 8, 8 if B > 2 else 2, 128, N, N - 8, 4)
 
@@ -270,9 +272,13 @@ def test_host_entry_point_matches_device(cuda_lib, B, N, mode, out_dtype):
     for _ in range(wl.steps):
         q, kn, vn = syn.step()
         c1.decode_step(q.cuda(), kn.cuda(), vn.cuda(), out, slot)
-        oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        sh = torch.empty(slot.shape, dtype=torch.int32).pin_memory()
-        c2.decode_step_host(q.pin_memory(), kn.pin_memory(), vn.pin_memory(), oh, sh)
+        oh = torch.empty(out.shape, dtype=out.dtype)
+        sh = torch.empty(slot.shape, dtype=torch.int32)
+        hin = (q, kn, vn)
+        if pinned:
+            oh, sh = oh.pin_memory(), sh.pin_memory()
+            hin = tuple(t.pin_memory() for t in hin)
+        c2.decode_step_host(*hin, oh, sh)
         torch.cuda.synchronize()
         assert torch.equal(oh, out.cpu())
         np.testing.assert_array_equal(sh.numpy(), slot.cpu().numpy())
