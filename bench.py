@@ -498,7 +498,9 @@ def main():
     d2h = oh.numel() * oh.element_size() + sh.numel() * 4
     e2e = {"value": B_total / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": h2d * args.gpus, "d2h_bytes_per_step": d2h * args.gpus,
-           "ms_per_step": float(e_ms.item()), "steps": e2e_steps, "api": "lf_decode_step_host"}
+           "ms_per_step": float(e_ms.item()), "steps": e2e_steps, "api": "lf_decode_step_host",
+           "io": ("pinned host buffers: the kernel reads q/k*/v* from and writes out/slot to them over the host "
+                  "link inside the timed step (zero-copy), then one stream sync")}
 
     out_bytes = 2 if args.out_dtype == "bf16" else 4
     alg = alg_bytes_per_step(wl, B, out_bytes)
