@@ -71,7 +71,8 @@ __host__ __device__ inline TcSmem tc_smem(int chunk, int stages, int kNG = kMaxN
     int off = 0;
     s.ring = off; off += stages * kStageBytes;   // 1024-aligned (swizzle atoms)
     s.q = off;    off += 2 * 4096;               // Q^T operand x2 (unit parity): 8 rows used
-    s.pbuf = off; off += kNG * 4096;             // P^T operand per group: 16 rows x 128 tokens
+    s.pbuf = off; off += (kNG > 1 ? kNG : 2) * 4096;   // P^T operand buffers (16 rows x 128 tokens):
+                                                      // one per group, two for a single group
     s.L = off;    off += chunk * 4;              // lambda_j of the current unit
     s.xb = off;   off += 2 * (int)sizeof(Xchg);
     s.misc = off; off += 512 * 4;                // scalars + per-rank combine factors [16][16]
@@ -215,6 +216,7 @@ __host__ __device__ inline int hold_tokens(int N, int chunk, bool solo) {
 template <int GP, int kNG, bool kLat>
 __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     constexpr int kNS = 128 * kNG;          // softmax threads
+    constexpr int kNPB = kNG > 1 ? kNG : 2; // P^T operand buffers (PREADY / PFREE barrier pairs)
     extern __shared__ unsigned char smem_raw[];
     const StepParams& p = a.p;
     // 1024-byte aligned base (swizzle atoms); offset arithmetic keeps the shared state space
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::mbar_init(BAR(FULL + i), 1);      // producer's expect_tx arrival
             ptx::mbar_init(BAR(EMPTY + i), 1);     // MMA commit (the MMA is each stage's last reader)
         }
-        for (int i = 0; i < kNG; ++i) {
+        for (int i = 0; i < kNPB; ++i) {
             ptx::mbar_init(BAR(PREADY + i), 4);
             ptx::mbar_init(BAR(PFREE + i), 1);
         }
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
     }
     if (warp >= 2) {   // zero the Q and P operand buffers (rows >= G stay zero)
         uint4* z = (uint4*)(smem + so.q);
-        for (int e = tid - 64; e < (2 + kNG) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
+        for (int e = tid - 64; e < (2 + kNPB) * 4096 / 16; e += kNS) z[e] = make_uint4(0, 0, 0, 0);
         ptx::fence_proxy_async_smem();
     }
     ptx::tc_fence_before();
@@ -469,8 +471,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
                     ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
-                    const int pb = pi % kNG;
-                    ptx::mbar_wait(BAR(PREADY + pb), (pi / kNG) & 1u);
+                    const int pb = pi % kNPB;
+                    ptx::mbar_wait(BAR(PREADY + pb), (pi / kNPB) & 1u);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
@@ -689,10 +691,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             for (int t = 0; t < x.ntiles; ++t) {
                 const uint32_t c = pi + t;
                 if ((int)(c % kNG) != grp) continue;
-                const int pb = c % kNG;
+                const int pb = c % kNPB;   // a single group alternates two P buffers, so it writes
+                                           // P of tile t+1 while the PV MMA of tile t still reads P(t)
                 uint32_t r[8];
                 ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNG) & 1u) ^ 1u);
+                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNPB) & 1u) ^ 1u);
                 ptx::tmem_ld_wait();
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
