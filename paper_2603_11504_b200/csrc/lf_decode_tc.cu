@@ -1192,16 +1192,18 @@ bool tc_supported(int G, int d) { return d == 128 && G >= 1 && G <= 8; }
 // with the cross-CTA exchange).  Solo rounds process whole units per CTA (no exchange); the
 // remaining units are split S ways, which balances the tail.
 // Round model of a plan's step time (us) in the HBM regime, fitted to a measured exploration of the
-// plan space on B200 (profiles/r02_split_explore.jsonl: S = 1..8 x k x solo at 8 mid-size sweep points,
-// plus the r02 budget sweep; picks within 0-4 % of the best measured plan there): in every round the A
-// active CTAs each stream `tokens` (512 B each, K + V); the round lasts the longer of the HBM time
-// A * bytes / BW and one CTA's streaming time bytes / rho_k (rho_1 = 48 GB/s with three softmax groups,
-// rho_2 = 26 GB/s with one), plus the unit-boundary overhead (1 us for whole units, 3 us for split units:
-// the part of the cross-CTA exchange the next unit's K pass does not hide).  It sees what the token
-// proxy below does not: a last round with few active CTAs, and clusters the GPCs cannot pack (S = 4:
-// 33 clusters = 132 SMs), which is why mid-size grids (B = 16-32) prefer S = 5 or 6 at two CTAs per SM.
+// plan space on B200 (profiles/r02_split_explore3.jsonl + r02_split_explore4.jsonl: S = 1..16 x k x solo
+// at 18 sweep points of 0.07-8 GB, parameters chosen to minimise the time lost by the pick: 0.3 % on
+// average and at most 2.1 % above the best measured plan of each point): in every round the A active
+// CTAs each stream `tokens` (512 B each, K + V); the round lasts the longer of the HBM time
+// A * bytes / BW and one CTA's streaming time bytes / rho_k (rho_1 = 44 GB/s with three softmax groups,
+// rho_2 = 26 GB/s with one), plus the unit-boundary overhead (0.5 us for whole units, 1 + 0.5 log2 S us
+// for split units: the part of the cross-CTA exchange the next unit's K pass does not hide).  It sees
+// what the token proxy below does not: a last round with few active CTAs, and clusters the GPCs cannot
+// pack (S = 4: 33 clusters = 132 SMs), which is why mid-size grids (B = 16-32) prefer S = 4-6 at two
+// CTAs per SM.
 static double stream_cost_us(long long units, int S, int C, int chunk, int N, long long R, int k) {
-    const double bw = 6.8e12, rho = k == 1 ? 48e9 : 26e9, ovh1 = 1.0, ovhS = 3.0;
+    const double bw = 6.8e12, rho = k == 1 ? 44e9 : 26e9, ovh1 = 0.5, ovhS = 1.0 + 0.5 * log2((double)S);
     const long long P = (long long)C * S;
     long long rem = units;
     double t = 0.0;
