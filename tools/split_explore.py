@@ -18,6 +18,9 @@ ap.add_argument("--points", default="32x4096,32x8192")
 ap.add_argument("--splits", default="0,1,2,3,4,5,6,7,8,12,16")
 ap.add_argument("--ks", default="1,2")
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--lat", default="auto", choices=["auto", "both"],
+                help="both: time split plans with and without the latency variant")
+ap.add_argument("--no-solo", action="store_true", help="skip the solo-round variants")
 ap.add_argument("--out", default="gpurun_out/split_explore.jsonl")
 args = ap.parse_args()
 peak, _ = peaks()
@@ -75,13 +78,14 @@ for pt in args.points.split(","):
         if S and -(-N // split) != S:
             continue
         for k in (map(int, args.ks.split(",")) if S else [0]):
-            for solo in ((None,) if S in (0, 1) else (False, True)):
-                kw = dict(split_tokens=split, ctas_per_sm=k, solo=solo)
-                try:
-                    rec = measure(B, N, **kw)
-                except LFError as e:
-                    print("no plan", B, N, kw, str(e)[:120], flush=True)
-                    continue
-                print(json.dumps(rec), flush=True)
-                f.write(json.dumps(rec) + "\n")
-                f.flush()
+            for solo in ((None,) if S in (0, 1) or args.no_solo else (False, True)):
+                for lat in ((None,) if S in (0, 1) or args.lat == "auto" else (False, True)):
+                    kw = dict(split_tokens=split, ctas_per_sm=k, solo=solo, latency_variant=lat)
+                    try:
+                        rec = measure(B, N, **kw)
+                    except LFError as e:
+                        print("no plan", B, N, kw, str(e)[:120], flush=True)
+                        continue
+                    print(json.dumps(rec), flush=True)
+                    f.write(json.dumps(rec) + "\n")
+                    f.flush()
