@@ -1222,6 +1222,36 @@ static double stream_cost_us(long long units, int S, int C, int chunk, int N, lo
     return t;
 }
 
+// Latency model of a plan's step time (us) for steps below 64 MB, fitted to a measured exploration of
+// the plan space on B200 (profiles/r02_lat_explore.jsonl: power-of-two S x k x latency variant at 20
+// sweep points of 2-67 MB; the pick is the best measured plan at every point): the same rounds as
+// stream_cost_us, but a CTA's streaming rate is 40 GB/s with three softmax groups and 34 GB/s with one
+// (a short chunk never reaches the steady state the HBM-regime rates describe), divided by 1.4 when two
+// CTAs share an SM; the exchange of a split unit adds 0.5 us, and the three-group CTA (448 threads,
+// all 512 TMEM columns) pays 1.5 us more per round than the one-group CTA -- which is why the small
+// sweep points take one-tile splits at two CTAs per SM (B = 2 N = 512: 10.3 -> 6.9 us).
+static double latency_cost_us(long long units, int S, int C, int chunk, int N, long long R, int k, int num_sms) {
+    const double bw = 6.8e12, rho = k == 1 ? 40e9 : 34e9, ovhS = 0.5, base = k == 1 ? 1.5 : 0.0;
+    const long long P = (long long)C * S;
+    long long rem = units;
+    double t = 0.0;
+    auto round = [&](long long A, double by, double ovh) {
+        const double r = (k == 2 && A > num_sms) ? rho / 1.4 : rho;
+        t += fmax((double)A * by / bw, by / r) * 1e6 + ovh + base;
+    };
+    for (long long r = 0; r < R && rem > 0; ++r) {
+        const long long A = rem < P ? rem : P;
+        round(A, (double)N * 512.0, 0.0);
+        rem -= A;
+    }
+    while (rem > 0) {
+        const long long c = rem < C ? rem : C;
+        round(c * S, (double)(chunk < N ? chunk : N) * 512.0, S > 1 ? ovhS : 0.0);
+        rem -= c;
+    }
+    return t;
+}
+
 Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, const PlanForce& force) {
     (void)d;
     Plan best;
@@ -1235,9 +1265,9 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
     best.tmem_cols = 0;
     best.solo_rounds = 0;
     const int Nr = (N + 127) / 128 * 128;
-    // Two regimes.  Steps that move >= 64 MB are HBM streams: the round model (stream_cost_us) over
+    // Three regimes.  Steps that move >= 64 MB are HBM streams: the round model (stream_cost_us) over
     // every cluster size S = 1..16.  Smaller steps are latency chains (q7, small sweep points): the
-    // token proxy below, tuned with the trace over power-of-two S in round 1.
+    // latency model (latency_cost_us) over power-of-two S.
     // Above 16 GB per step the round model's 9-CTA two-per-SM picks measured worse than the token
     // proxy's S = 4 in long runs (512 x 16384: 0.87 vs 0.98 of the copy peak; 256 x 16384: 2.92 vs
     // 2.72 ms under the power cap, profiles/r02_ab_planner.txt), so the proxy keeps the largest steps.
@@ -1301,6 +1331,7 @@ Plan tc_plan(int units, int G, int d, int N, int split_tokens, int num_sms, cons
                     cost = (double)(((units + Cu - 1) / Cu) * ((long long)k * chunk + ovhS / k));
                 }
                 if (hbm_regime) cost = stream_cost_us(units, splits, C, chunk, N, R, k);
+                else if (step_bytes < 64e6) cost = latency_cost_us(units, splits, C, chunk, N, R, k, num_sms);
                 if (best_cost < 0 || cost < best_cost) {
                     best_cost = cost;
                     best.splits = splits;

@@ -34,6 +34,9 @@ if "--flush" in sys.argv:   # cold L2 / TLB, as bench.py times L2-resident confi
 cache.decode_step(q, kn, vn, out, slot)
 torch.cuda.synchronize()
 a = tr.view(ctas, 64, 32).cpu().numpy().astype(np.int64)
+raw0 = a[0, 0, :31].copy()   # CTA 0, first item: raw SM cycles (clock granularity check)
+rv = raw0[raw0 > 0]
+print("CTA 0 raw cycle offsets from entry:", sorted((rv - a[0, 0, 16]).tolist()))
 # events are SM cycles; row 0 slot 16 = entry cycles, slot 31 = entry globaltimer (ns)
 ghz = float(os.environ.get("LF_TRACE_GHZ", "1.965"))
 for c in range(ctas):
@@ -86,7 +89,7 @@ rel_names = {16: "entry", 17: "csync", 18: "pdlw", 19: "pdlw(softmax)", 20: "sm_
              22: "prod_n_loaded", 24: "prod_qfree", 6: "prodQ", 7: "mmaQ", 0: "start", 15: "xsdone",
              1: "maxdone", 5: "Vland", 2: "Vdone", 8: "xfree", 9: "ofull", 10: "ostage", 11: "pushed",
              3: "xready", 12: "MZ", 4: "keypush", 13: "comb", 14: "r0done"}
-r0 = a[used][:, 0].astype(np.float64)
+r0 = a[used[:, 0], 0].astype(np.float64)
 ok0 = r0[:, 18] > 0
 print("first item, us after the CTA's own PDL wait (mean over CTAs):")
 for j, nm in rel_names.items():
