@@ -1,11 +1,12 @@
 // tcgen05.mma issue-rate probe (tuning aid): cycles per kind::f16 MMA (K=16, SW128 K-major A and B from
-// SMEM, fp32 accumulate in TMEM) for the decode kernel's shapes and their transposes.
+// SMEM, fp32 accumulate in TMEM) for the decode kernel's shapes and their transposes.  NACC > 1: the MMAs
+// rotate over NACC accumulators (independent chains) instead of all accumulating into one.
 #include <cuda_runtime.h>
 #include <cstdio>
 #include "lf_tc_ptx.cuh"
 using namespace lf;
 
-template <int M, int N, int kAMN>
+template <int M, int N, int kAMN, int NACC>
 __global__ void __launch_bounds__(128, 1) mma_rate(int reps, long long* out) {
     extern __shared__ unsigned char smem_raw[];
     unsigned char* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -30,7 +31,7 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int reps, long long* out) {
                 const uint64_t da = kAMN ? ptx::smem_desc_sw128(a + kk * 2048, 16384, 1024)
                                          : ptx::smem_desc_sw128(a + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024);
                 const uint64_t db = ptx::smem_desc_sw128(b + (kk >> 2) * 32768 + (kk & 3) * 32, 16, 1024);
-                ptx::mma_bf16(tmem, da, db, idesc, (r | kk) > 0);
+                ptx::mma_bf16(tmem + (uint32_t)((kk % NACC) * (N < 16 ? 16 : N)), da, db, idesc, (r | (kk / NACC)) > 0);
             }
         }
         ptx::mma_commit(bar);
@@ -45,16 +46,16 @@ __global__ void __launch_bounds__(128, 1) mma_rate(int reps, long long* out) {
     }
 }
 
-template <int M, int N, int kAMN>
+template <int M, int N, int kAMN, int NACC = 1>
 void run(long long* d) {
-    cudaFuncSetAttribute(mma_rate<M, N, kAMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+    cudaFuncSetAttribute(mma_rate<M, N, kAMN, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     const int reps = 64;
-    for (int i = 0; i < 2; ++i) mma_rate<M, N, kAMN><<<1, 128, 140 * 1024>>>(reps, d);
+    for (int i = 0; i < 2; ++i) mma_rate<M, N, kAMN, NACC><<<1, 128, 140 * 1024>>>(reps, d);
     cudaDeviceSynchronize();
     long long h;
     cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
     const double per = (double)h / (reps * 8);
-    printf("M%3d N%3d A %s: %6.1f cycles per MMA  (%.0f FMA/cycle, A+B %d B per MMA)  err=%s\n", M, N,
+    printf("NACC %d M%3d N%3d A %s: %6.1f cycles per MMA  (%.0f FMA/cycle, A+B %d B per MMA)  err=%s\n", NACC, M, N,
            kAMN ? "MN-major" : "K-major ", per, (double)M * N * 16 / per, (M + N) * 32,
            cudaGetErrorString(cudaGetLastError()));
 }
@@ -74,5 +75,11 @@ int main() {
     run<64, 64, 0>(d);
     run<64, 128, 0>(d);
     run<64, 256, 0>(d);
+    run<128, 8, 0, 2>(d);
+    run<128, 8, 0, 4>(d);
+    run<128, 8, 0, 8>(d);
+    run<128, 16, 1, 2>(d);
+    run<128, 16, 1, 4>(d);
+    run<128, 16, 1, 8>(d);
     return 0;
 }

@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(128, 1) probe_c(const unsigned char* g, int S,
                     const uint64_t db = ptx::smem_desc_sw128(qb + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 1024);
                     ptx::mma_bf16(tmem + 8u * (it & 3), da, db, idesc, kk > 0);
                 }
-                ptx::mma_commit(empty + 8 * st);
+                if (kMma == 1) ptx::mma_commit(empty + 8 * st);
+                else ptx::mbar_arrive(empty + 8 * st);   // kMma 2: stage released at issue (timing only)
             } else {
                 ptx::mbar_arrive(empty + 8 * st);
             }
@@ -248,8 +249,8 @@ int main() {
             printf("\n");
         }
     }
-    for (int m = 0; m < 2; ++m) {
-        auto k = m ? probe_c<1> : probe_c<0>;
+    for (int m = 0; m < 3; ++m) {
+        auto k = m == 2 ? probe_c<2> : m ? probe_c<1> : probe_c<0>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         for (int S : {2, 4, 6}) {
             for (int rep = 0; rep < 2; ++rep) {
@@ -258,7 +259,7 @@ int main() {
             }
             long long h[64];
             cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
-            printf("ring+%s S=%d: cycles per stage over 8..63: %.0f\n", m ? "QK-MMA" : "no-MMA", S, (h[63] - h[7]) / 56.0);
+            printf("ring+%s S=%d: cycles per stage over 8..63: %.0f\n", m == 2 ? "QK-MMA(release at issue)" : m ? "QK-MMA" : "no-MMA", S, (h[63] - h[7]) / 56.0);
         }
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
