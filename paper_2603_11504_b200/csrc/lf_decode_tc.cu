@@ -153,6 +153,14 @@ __device__ __forceinline__ float row_l1(const unsigned char* Vt, int row) {
     return a0 + a1;
 }
 
+// min of a 64-bit (score bits, slot) key over the warp: two REDUX.MIN instead of five 64-bit shuffle
+// rounds (exact: the high word decides, the low word breaks ties among the lanes holding that high word)
+__device__ __forceinline__ unsigned long long warp_min_key(unsigned long long k) {
+    const uint32_t hi = ptx::warp_min_u32((uint32_t)(k >> 32));
+    const uint32_t lo = ptx::warp_min_u32((uint32_t)(k >> 32) == hi ? (uint32_t)k : 0xffffffffu);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
 struct UnitInfo {
     int u, b, h, n, c0, c1, nv, ntiles;
     bool split, valid;
@@ -214,7 +222,8 @@ __host__ __device__ inline int hold_tokens(int N, int chunk, bool solo) {
 // computed while its QK MMA runs.  Machine-filling and single-CTA-per-unit plans use kLat = false,
 // the streaming-tuned code (measured: the latency changes cost 1-3 % there).
 template <int GP, int kNG, bool kLat>
-__global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
+// (the one-group variant must fit two CTAs per SM: <= 170 registers, enforced by the launch bound)
+__global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_kernel(const __grid_constant__ TcArgs a) {
     constexpr int kNS = 128 * kNG;          // softmax threads
     constexpr int kNPB = kNG > 1 ? kNG : 2; // P^T operand buffers (PREADY / PFREE barrier pairs)
     extern __shared__ unsigned char smem_raw[];
@@ -474,6 +483,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     const int pb = pi % kNPB;
                     ptx::mbar_wait(BAR(PREADY + pb), (pi / kNPB) & 1u);
                     ptx::tc_fence_after();
+                    if (t == 0) LF_EVENT(ui, 28);
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
 #pragma unroll
@@ -486,6 +496,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                     ptx::mma_commit(BAR(PFREE + pb));
                 }
                 ptx::mma_commit(BAR(OFULL));
+                LF_EVENT(ui, 29);
             }
         }
         __syncwarp();
@@ -510,7 +521,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
         const float sl2 = p.scale_log2;
         // scores I_j (Eq. 6, mean over the group) of this thread's tokens from the TMEM logits and the
         // local argmin key (ordered log2 I_j, slot); needs gM, glz of the unit
-        auto unit_scores = [&](const UnitInfo& x, int u, uint32_t sreg) -> unsigned long long {
+        // s_reg: the logits of tile 0 already in registers (one-tile CTAs of the one-group variant) or nullptr
+        auto unit_scores = [&](const UnitInfo& x, int u, uint32_t sreg, const uint32_t* s_reg) -> unsigned long long {
             const int nv = x.nv;
             unsigned long long best = ~0ull;
             const int excl = (p.deferred && p.exclude_newest) ? __ldg(p.written + u) : -1;
@@ -519,8 +531,13 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             for (int g = 0; g < GP; ++g) wM[g] = g < G ? gM[g] + glz[g] : 0.f;
             for (int t = grp; t < x.ntiles; t += kNG) {
                 uint32_t r[8];
-                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::tmem_ld_wait();
+                if (s_reg) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) r[g] = s_reg[g];
+                } else {
+                    ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
+                    ptx::tmem_ld_wait();
+                }
                 const int j = t * 128 + row;
                 if (j < nv) {
                     const float lam = Ls[j];
@@ -650,13 +667,22 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             // ---- max over the unit's logits (TMEM-resident S)
             ptx::mbar_wait(BAR(KDONE + par), (ui >> 1) & 1u);
             ptx::tc_fence_after();
+            if (sidx == 0) LF_EVENT(ui, 30);
             float mloc[GP];
 #pragma unroll
             for (int g = 0; g < GP; ++g) mloc[g] = -INFINITY;
+            // one-tile CTA of the one-group variant: its logits stay in registers for the V pass and the
+            // scores (two TMEM round trips less on the latency chain)
+            const bool s_in_regs = kNG == 1 && lam_first;
+            uint32_t s0[8];
             for (int t = grp; t < x.ntiles; t += kNG) {
                 uint32_t r[8];
                 ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
                 ptx::tmem_ld_wait();
+                if (s_in_regs) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) s0[g] = r[g];
+                }
                 if (t * 128 + row < nv) {
 #pragma unroll
                     for (int g = 0; g < GP; ++g)
@@ -664,10 +690,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 }
             }
 #pragma unroll
-            for (int g = 0; g < GP; ++g) {
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) mloc[g] = fmaxf(mloc[g], __shfl_xor_sync(0xffffffffu, mloc[g], off));
-            }
+            for (int g = 0; g < GP; ++g) mloc[g] = ptx::warp_max_f32(mloc[g]);
             if (lane == 0) {
 #pragma unroll
                 for (int g = 0; g < GP; ++g) red[(grp * 4 + q4) * 16 + g] = mloc[g];
@@ -680,7 +703,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 m[g] = red[g];
 #pragma unroll
                 for (int w = 1; w < 4 * kNG; ++w) m[g] = fmaxf(m[g], red[w * 16 + g]);
+                if (g >= G) m[g] = 0.f;   // padded heads: logits exactly 0 (zero Q rows), P = 1, never read
             }
+            if (sidx == 0) LF_EVENT(ui, 23);
             // ---- V pass: P (hi/lo bf16) for the MMA, Z, lambda
             float z[GP];
 #pragma unroll
@@ -694,23 +719,31 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 const int pb = c % kNPB;   // a single group alternates two P buffers, so it writes
                                            // P of tile t+1 while the PV MMA of tile t still reads P(t)
                 uint32_t r[8];
-                ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
-                ptx::mbar_wait(BAR(PFREE + pb), ((c / kNPB) & 1u) ^ 1u);
-                ptx::tmem_ld_wait();
+                if (s_in_regs) {
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) r[g] = s0[g];
+                    ptx::mbar_wait(BAR(PFREE + pb), ((c / kNPB) & 1u) ^ 1u);
+                } else {
+                    ptx::tmem_ld_x8(sreg + 8u * (uint32_t)t, r);
+                    ptx::mbar_wait(BAR(PFREE + pb), ((c / kNPB) & 1u) ^ 1u);
+                    ptx::tmem_ld_wait();
+                }
+                if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 25);
                 const int tok = t * 128 + row;
                 const bool valid = tok < nv;
                 unsigned char* P = smem + so.pbuf + pb * 4096 + box * 2048;
+                // every head of the padded group, no per-head branch: padded heads (g >= G) get P = 1
+                // from their zero logits, feed only O^T columns nobody reads, and their z is never used
 #pragma unroll
                 for (int g = 0; g < GP; ++g) {
-                    if (g < G) {
-                        const float pv = valid ? ptx::ex2_approx(__uint_as_float(r[g]) * sl2 - m[g]) : 0.f;
-                        z[g] += pv;
-                        const uint16_t hi = ptx::cvt_bf16_rn(pv);   // hardware RNE (pv is finite)
-                        const uint16_t lo = ptx::cvt_bf16_rn(pv - bf16_to_f32(hi));
-                        *(uint16_t*)(P + g * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = hi;
-                        *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
-                    }
+                    const float pv = valid ? ptx::ex2_approx(__uint_as_float(r[g]) * sl2 - m[g]) : 0.f;
+                    z[g] += pv;
+                    const uint16_t hi = ptx::cvt_bf16_rn(pv);   // hardware RNE (pv is finite)
+                    const uint16_t lo = ptx::cvt_bf16_rn(pv - bf16_to_f32(hi));
+                    *(uint16_t*)(P + g * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = hi;
+                    *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
                 }
+                if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 26);
                 const uint32_t iv = it + x.ntiles + t;
                 const int st = iv % ST;
                 if (!lam_first) {
@@ -734,6 +767,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                 Ls[tok] = lam;
                 }
                 ptx::fence_proxy_async_smem();
+                if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 27);
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(PREADY + pb));
                 if (lane == 0 && q4 == 0) LF_TILE_EVENT(ui, 33, t);
@@ -790,14 +824,14 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         }
                     }
                 }
-                unsigned long long best = unit_scores(x, u, sreg);
+                unsigned long long best = unit_scores(x, u, sreg, s_in_regs ? s0 : nullptr);
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(BAR(SFREE + par));
                 if (p.scores)
                     for (int j = nv + sidx; j < x.c1 - x.c0; j += kNS) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
 #pragma unroll
-                for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
+                best = warp_min_key(best);
                 if (lane == 0) kred[warp - 2] = best;
                 ptx::named_bar_sync(1, kNS);
                 if (sidx == 0) {
@@ -903,9 +937,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         if (r == 0) {
                             gM[g] = M;
                             gZ[g] = Z;
-                            glz[g] = log2f(Z);
+                            glz[g] = ptx::lg2_approx(Z);   // Z >= 1 (the max term); same bits on every rank
                             gFn[g] = fn;
-                            gIZ[g] = 1.0f / Z;
+                            gIZ[g] = __frcp_rn(Z);
                         }
                     }
                 }
@@ -935,14 +969,14 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
             ptx::named_bar_sync(1, kNS);
             if (sidx == 0) LF_EVENT(ui, 12);
             // ---- scores I_j (Eq. 6, mean over the group) from the TMEM logits; local argmin key
-            unsigned long long best = unit_scores(x, u, sreg);
+            unsigned long long best = unit_scores(x, u, sreg, s_in_regs ? s0 : nullptr);
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(BAR(SFREE + par));          // S(ui) no longer read
             if (p.scores)
                 for (int j = nv + sidx; j < x.c1 - x.c0; j += kNS) p.scores[(size_t)u * N + x.c0 + j] = INFINITY;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) best = umin64(best, __shfl_xor_sync(0xffffffffu, best, off));
+            best = warp_min_key(best);
             if (lane == 0) kred[warp - 2] = best;
             ptx::named_bar_sync(1, kNS);
             if (sidx == 0) {   // key -> rank 0's inbox, then release to rank 0
@@ -962,14 +996,16 @@ __global__ void __launch_bounds__(64 + 128 * kNG, 1) tc_decode_kernel(const __gr
                         const int i4 = i4_0 + e;
                         const int g = i4 >> 5, l = (i4 & 31) * 4;
                         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-                        for (int r = 0; r < S; ++r) {
-                            const float f = fr[g * 16 + r];
-                            const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
-                            acc.x = fmaf(o4.x, f, acc.x);
-                            acc.y = fmaf(o4.y, f, acc.y);
-                            acc.z = fmaf(o4.z, f, acc.z);
-                            acc.w = fmaf(o4.w, f, acc.w);
+#pragma unroll 8
+                        for (int r = 0; r < 16; ++r) {   // predicated, so the inbox loads issue together
+                            if (r < S) {
+                                const float f = fr[g * 16 + r];
+                                const float4 o4 = *(const float4*)(xc->o + 4 * (r * E4 + e));
+                                acc.x = fmaf(o4.x, f, acc.x);
+                                acc.y = fmaf(o4.y, f, acc.y);
+                                acc.z = fmaf(o4.z, f, acc.z);
+                                acc.w = fmaf(o4.w, f, acc.w);
+                            }
                         }
                         const float fn = gFn[g], invZ = gIZ[g];
                         const uint2 vw = *(const uint2*)(vn + l);

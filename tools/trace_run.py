@@ -31,7 +31,11 @@ cache.set_trace(tr)
 if "--flush" in sys.argv:   # cold L2 / TLB, as bench.py times L2-resident configs
     fl = torch.zeros(128 << 20, dtype=torch.float32, device="cuda")
     fl.amax()
-cache.decode_step(q, kn, vn, out, slot)
+# --b2b K: K back-to-back steps without a sync (PDL overlaps each step's prologue with the previous
+# step); the trace keeps the events of the last one (every step writes the same slots)
+b2b = int(sys.argv[sys.argv.index("--b2b") + 1]) if "--b2b" in sys.argv else 1
+for _ in range(b2b):
+    cache.decode_step(q, kn, vn, out, slot)
 torch.cuda.synchronize()
 a = tr.view(ctas, 64, 32).cpu().numpy().astype(np.int64)
 raw0 = a[0, 0, :31].copy()   # CTA 0, first item: raw SM cycles (clock granularity check)
@@ -88,11 +92,12 @@ if per_cta:
 rel_names = {16: "entry", 17: "csync", 18: "pdlw", 19: "pdlw(softmax)", 20: "sm_base", 21: "sm_n_loaded",
              22: "prod_n_loaded", 24: "prod_qfree", 6: "prodQ", 7: "mmaQ", 0: "start", 15: "xsdone",
              1: "maxdone", 5: "Vland", 2: "Vdone", 8: "xfree", 9: "ofull", 10: "ostage", 11: "pushed",
-             3: "xready", 12: "MZ", 4: "keypush", 13: "comb", 14: "r0done"}
+             3: "xready", 12: "MZ", 4: "keypush", 13: "comb", 14: "r0done", 30: "kdone_seen", 23: "m_ready",
+             25: "S_loaded(V)", 26: "P_stored", 27: "P_fenced", 28: "mma_PREADY", 29: "mma_PV_committed"}
 r0 = a[used[:, 0], 0].astype(np.float64)
 ok0 = r0[:, 18] > 0
 print("first item, us after the CTA's own PDL wait (mean over CTAs):")
-for j, nm in rel_names.items():
+for j, nm in sorted(rel_names.items(), key=lambda kv: np.mean(r0[ok0 & (r0[:, kv[0]] > 0), kv[0]] - r0[ok0 & (r0[:, kv[0]] > 0), 18]) if (ok0 & (r0[:, kv[0]] > 0)).any() else 1e18):
     m = ok0 & (r0[:, j] > 0)
     if m.any():
-        print(f"  {nm:14s} {np.mean(r0[m, j] - r0[m, 18]) / 1e3:7.3f}")
+        print(f"  {nm:16s} {np.mean(r0[m, j] - r0[m, 18]) / 1e3:7.3f}  ({np.mean(r0[m, j] - r0[m, 18]) * ghz:7.0f} cycles)")
