@@ -5,7 +5,7 @@
 # first (the recipe's rule).  usage: bash tools/ncu_round.sh <tag>
 T=${1:-r2}
 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/${T}_launches_r.csv \
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:decode -c 40 --csv --log-file gpurun_out/${T}_launches_r.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 for w in r q3 q7 f1 sweep_b128_n512 sweep_b32_n8192; do
   extra=""; [ $w = sweep_b128_n512 ] && extra="--ctas-per-sm 2"
