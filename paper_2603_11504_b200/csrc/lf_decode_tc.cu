@@ -442,7 +442,13 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
         }
     } else if (warp == 1) {
         // ------------------------------ MMA issuer -----------------------------------------------
-        if (lane == 0) {
+        // The whole warp walks the issue loop (converged, so the loop state and the descriptors live on
+        // the uniform datapath) and one elected lane issues each tile's eight MMAs and its commits as one
+        // block: round 1 ran the loop on lane 0 alone, and the compiler then wrapped EVERY tcgen05.mma in
+        // a waterfall loop (ELECT / R2UR / BRA.U.ANY, ~16 instructions per MMA) -- measured, the MMA issue
+        // rate bounded one CTA's K pass (0.42 -> 0.37 us per tile with the descriptors built once per
+        // tile, profiles/r02_ab_mma_issue.txt).
+        {
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
             uint32_t it = 0, pi = 0, ui = 0;
@@ -466,16 +472,26 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     LF_TILE_EVENT(ui, 32, t);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
+                    // descriptors built once per tile; the K steps only advance the 14-bit start-address
+                    // field (address / 16; every SMEM address < 228 KB fits, so the add never carries)
+                    const uint64_t da0 = ptx::smem_desc_sw128(base, 16, 1024);
+                    const uint64_t db0 = ptx::smem_desc_sw128(qbase, 16, 1024);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t da = ptx::smem_desc_sw128(base + (kk >> 2) * kBoxBytes + (kk & 3) * 32, 16, 1024);
-                        const uint64_t db = ptx::smem_desc_sw128(qbase + (kk >> 2) * 1024 + (kk & 3) * 32, 16, 1024);
-                        ptx::mma_bf16(sreg + 8u * (uint32_t)t, da, db, idesc_qk, kk > 0);
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t da = da0 + (uint64_t)((kk >> 2) * (kBoxBytes >> 4) + (kk & 3) * 2);
+                            const uint64_t db = db0 + (uint64_t)((kk >> 2) * 64 + (kk & 3) * 2);
+                            ptx::mma_bf16(sreg + 8u * (uint32_t)t, da, db, idesc_qk, kk > 0);
+                        }
+                        ptx::mma_commit(BAR(EMPTY + st));
                     }
-                    ptx::mma_commit(BAR(EMPTY + st));
+                    __syncwarp();
                 }
-                ptx::mma_commit(BAR(QFREE + par));
-                ptx::mma_commit(BAR(KDONE + par));
+                if (ptx::elect_one()) {
+                    ptx::mma_commit(BAR(QFREE + par));
+                    ptx::mma_commit(BAR(KDONE + par));
+                }
+                __syncwarp();
                 const uint32_t oreg = tmem + (par ^ 1u) * RC;
                 for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
                     const int st = it % ST;
@@ -486,16 +502,22 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     if (t == 0) LF_EVENT(ui, 28);
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
                     const uint32_t pbase = pbuf + (uint32_t)pb * 4096;
+                    const uint64_t da0 = ptx::smem_desc_sw128(base, kBoxBytes, 1024);
+                    const uint64_t db0 = ptx::smem_desc_sw128(pbase, 16, 1024);
+                    if (ptx::elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const uint64_t da = ptx::smem_desc_sw128(base + kk * 2048, kBoxBytes, 1024);
-                        const uint64_t db = ptx::smem_desc_sw128(pbase + (kk >> 2) * 2048 + (kk & 3) * 32, 16, 1024);
-                        ptx::mma_bf16(oreg, da, db, idesc_pv, (t | kk) > 0);
+                        for (int kk = 0; kk < 8; ++kk) {
+                            const uint64_t da = da0 + (uint64_t)(kk * 128);
+                            const uint64_t db = db0 + (uint64_t)((kk >> 2) * 128 + (kk & 3) * 2);
+                            ptx::mma_bf16(oreg, da, db, idesc_pv, (t | kk) > 0);
+                        }
+                        ptx::mma_commit(BAR(EMPTY + st));
+                        ptx::mma_commit(BAR(PFREE + pb));
                     }
-                    ptx::mma_commit(BAR(EMPTY + st));
-                    ptx::mma_commit(BAR(PFREE + pb));
+                    __syncwarp();
                 }
-                ptx::mma_commit(BAR(OFULL));
+                if (ptx::elect_one()) ptx::mma_commit(BAR(OFULL));
+                __syncwarp();
                 LF_EVENT(ui, 29);
             }
         }

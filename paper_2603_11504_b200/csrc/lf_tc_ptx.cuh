@@ -217,6 +217,13 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+// one lane of the (converged) warp: elect.sync -- lets the compiler issue a block of tcgen05 ops with
+// uniform operands under ONE elect instead of a per-instruction waterfall loop
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "=r"(pred));
+    return pred != 0;
+}
 // max over the 32 lanes of the warp in one instruction (sm_100a CREDUX.MAX.F32; exact, NaN-ignoring
 // like fmaxf)
 __device__ __forceinline__ float warp_max_f32(float v) {
