@@ -168,7 +168,25 @@ __global__ void __launch_bounds__(128, 1) probe_c(const unsigned char* g, int S,
             ptx::mbar_arrive_expect_tx(full + 8 * st, sb);
             bulk_load_1d(ring + st * sb, g + (size_t)(it * sb % region), sb, full + 8 * st);
         }
-    } else if (threadIdx.x == 32) {
+    } else if (kMma == 3 && warp == 1) {   // the whole warp walks the loop, one elected lane issues
+        constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 8, 0, 0);
+        for (int it = 0; it < iters; ++it) {
+            const int st = it % S;
+            ptx::mbar_wait(full + 8 * st, (it / S) & 1);
+            if (it < 64 && lane == 0) out[it] = clock64() - t0;
+            ptx::tc_fence_after();
+            const uint32_t base = ring + st * sb;
+            const uint64_t da0 = ptx::smem_desc_sw128(base, 16, 1024), db0 = ptx::smem_desc_sw128(qb, 16, 1024);
+            if (ptx::elect_one()) {
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk)
+                    ptx::mma_bf16(tmem + 8u * (it & 3), da0 + (uint64_t)((kk >> 2) * 1024 + (kk & 3) * 2),
+                                  db0 + (uint64_t)((kk >> 2) * 64 + (kk & 3) * 2), idesc, kk > 0);
+                ptx::mma_commit(empty + 8 * st);
+            }
+            __syncwarp();
+        }
+    } else if (kMma != 3 && threadIdx.x == 32) {
         constexpr uint32_t idesc = ptx::idesc_bf16_f32(128, 8, 0, 0);
         for (int it = 0; it < iters; ++it) {
             const int st = it % S;
@@ -249,8 +267,8 @@ int main() {
             printf("\n");
         }
     }
-    for (int m = 0; m < 3; ++m) {
-        auto k = m == 2 ? probe_c<2> : m ? probe_c<1> : probe_c<0>;
+    for (int m = 0; m < 4; ++m) {
+        auto k = m == 3 ? probe_c<3> : m == 2 ? probe_c<2> : m ? probe_c<1> : probe_c<0>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         for (int S : {2, 4, 6}) {
             for (int rep = 0; rep < 2; ++rep) {
@@ -259,7 +277,7 @@ int main() {
             }
             long long h[64];
             cudaMemcpy(h, d, 64 * 8, cudaMemcpyDeviceToHost);
-            printf("ring+%s S=%d: cycles per stage over 8..63: %.0f\n", m == 2 ? "QK-MMA(release at issue)" : m ? "QK-MMA" : "no-MMA", S, (h[63] - h[7]) / 56.0);
+            printf("ring+%s S=%d: cycles per stage over 8..63: %.0f\n", m == 3 ? "QK-MMA(warp + elect)" : m == 2 ? "QK-MMA(release at issue)" : m ? "QK-MMA" : "no-MMA", S, (h[63] - h[7]) / 56.0);
         }
     }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
