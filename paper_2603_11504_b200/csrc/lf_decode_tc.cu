@@ -1281,15 +1281,16 @@ static double stream_cost_us(long long units, int S, int C, int chunk, int N, lo
 }
 
 // Latency model of a plan's step time (us) for steps below 64 MB, fitted to a measured exploration of
-// the plan space on B200 (profiles/r02_lat_explore.jsonl: power-of-two S x k x latency variant at 20
-// sweep points of 2-67 MB; the pick is the best measured plan at every point): the same rounds as
-// stream_cost_us, but a CTA's streaming rate is 40 GB/s with three softmax groups and 34 GB/s with one
-// (a short chunk never reaches the steady state the HBM-regime rates describe), divided by 1.4 when two
-// CTAs share an SM; the exchange of a split unit adds 0.5 us, and the three-group CTA (448 threads,
+// the plan space on B200 (profiles/r02_lat_explore2.jsonl, refitted after the MMA-issue change: power-of-
+// two S x k x latency variant at 20 sweep points of 2-67 MB; the pick is the best measured plan at every
+// point): the same rounds as stream_cost_us, but a CTA's streaming rate is 40 GB/s with three softmax
+// groups and 30 GB/s with one (a short chunk never reaches the steady state the HBM-regime rates
+// describe), divided by 1.4 when two CTAs share an SM; the exchange of a split unit adds 0.25 us, and the
+// three-group CTA (448 threads,
 // all 512 TMEM columns) pays 1.5 us more per round than the one-group CTA -- which is why the small
 // sweep points take one-tile splits at two CTAs per SM (B = 2 N = 512: 10.3 -> 6.9 us).
 static double latency_cost_us(long long units, int S, int C, int chunk, int N, long long R, int k, int num_sms) {
-    const double bw = 6.8e12, rho = k == 1 ? 40e9 : 34e9, ovhS = 0.5, base = k == 1 ? 1.5 : 0.0;
+    const double bw = 6.8e12, rho = k == 1 ? 40e9 : 30e9, ovhS = 0.25, base = k == 1 ? 1.5 : 0.0;
     const long long P = (long long)C * S;
     long long rem = units;
     double t = 0.0;
