@@ -932,7 +932,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 }
             }
             if (sidx == 0) LF_EVENT(ui, 11);
-            ptx::mbar_wait_cluster(xr_local, use & 1u);                 // every sender's bytes landed
+            // every sender's bytes landed: they arrive by st.async complete_tx into this CTA's own shared
+            // memory, which the CTA-scope wait makes visible (no cluster acquire, no L1 invalidation)
+            ptx::mbar_wait(xr_local, use & 1u);
             if (sidx == 0) LF_EVENT(ui, 3);
             // ---- global M_g, Z_g over the ranks (same order everywhere) + the current token
             float* fr = misc + 128;    // [g][r] = 2^(m_g,r - M_g)
@@ -1094,7 +1096,7 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
             if (sidx == 0) LF_EVENT(ui, 13);
             if (s == 0) {
                 // ---- rank 0: slot and the in-place eviction write
-                ptx::mbar_wait_cluster(BAR(KREADY + xp), use & 1u);
+                ptx::mbar_wait(BAR(KREADY + xp), use & 1u);   // keys arrive by st.async complete_tx
                 if (sidx == 0) {
                     unsigned long long mk = ~0ull;
                     for (int r = 0; r < S; ++r) mk = umin64(mk, xc->key[r]);
@@ -1119,7 +1121,11 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
             }
             ptx::named_bar_sync(1, kNS);   // my inbox of unit u is consumed
             if (sidx == 0) LF_EVENT(ui, 14);
-            if (sidx < S) ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));   // senders may reuse it
+            // senders may reuse the inbox -- unless this was the cluster's last unit (every CTA of the
+            // cluster walks the same unit list), where nobody waits and the release arrive would cost a
+            // GPU-scope fence on the way to the exit
+            if (sidx < S && item_base(p, cid, s, C, i + 1).valid)
+                ptx::mbar_arrive_remote(ptx::mapa(BAR(XFREE + xp), sidx));
         }
         // (no drain of the last XFREE phases: the cluster barrier below orders every CTA's remote
         // arrivals and stores before any CTA of the cluster leaves)
@@ -1128,7 +1134,17 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
     // every CTA of the cluster leaves together: no CTA exits while a peer may still address its shared
     // memory (round 1 drained its own XFREE phases instead; compute-sanitizer synccheck reported unsafe
     // exits for clusters of >= 4 CTAs placed two per SM, with illegal-address faults under the tool)
-    ptx::cluster_sync_all();
+    {
+        // split units this cluster computed (identical for its CTAs): with at most one, no CTA sent a
+        // remote XFREE arrive (the last unit's are skipped) and every remote write into a CTA landed
+        // before it got here, so the barrier needs no release half (no GPU-scope fence on the exit
+        // path: the latency variant's single-unit clusters); otherwise the release orders the earlier
+        // units' remote arrives before any CTA leaves
+        const int rest = p.B * p.Hkv - p.solo_units - cid;
+        const int nsplit = S > 1 && rest > 0 ? (rest + C - 1) / C : 0;
+        if (nsplit <= 1) ptx::cluster_sync_relaxed();
+        else ptx::cluster_sync_all();
+    }
     if (warp == 1) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc(tmem, (uint32_t)a.tmem_cols);

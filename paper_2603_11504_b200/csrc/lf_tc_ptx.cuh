@@ -203,6 +203,12 @@ __device__ __forceinline__ void st_async_u64(uint32_t cluster_addr, unsigned lon
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// cluster barrier without the release half (no MEMBAR.GPU before the arrive): for the end of the
+// kernel, where it only has to keep every CTA's shared memory alive until no peer can address it
+// (every remote write into a CTA has landed before that CTA arrives: it waited for their bytes)
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\nbarrier.cluster.wait.aligned;" ::: "memory");
+}
 
 // fp32 -> bf16 round-to-nearest-even in one instruction (F2FP); identical to the software RNE for
 // finite inputs (NaN encodings differ)
