@@ -894,7 +894,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 if (s == 0) ptx::mbar_arrive_expect_tx(BAR(KREADY + xp), (uint32_t)(S * 8));
             }
             const uint32_t xr_local = BAR(XREADY + xp);
-            ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // every receiver consumed use-1
+            if (use > 0)   // (the first use of each inbox parity has nothing to wait for)
+                ptx::mbar_wait_cluster(BAR(XFREE + xp), (use & 1u) ^ 1u);   // every receiver consumed use-1
             if (sidx == 0) LF_EVENT(ui, 8);
             if (grp == 0) {   // group 0 drains O (TMEM lane = d)
                 ptx::mbar_wait(BAR(OFULL), ui & 1u);
