@@ -20,11 +20,12 @@
 //           bf16 P alone misses the 2e-3 out bar); O^T[128 d x 16] += V^T . P^T
 //           (M=128, N=16, K=16 tokens per MMA, A MN-major straight from the TMA tile);
 //           lambda_j = ||v_j||_1 from the same tile on the CUDA cores (Eq. 6, R9).
-//   exchange (no cluster-wide barrier): each CTA publishes (m_g, Z_g, o_g) in SMEM and arrives on
-//           every rank's `xready`; all ranks compute M_g, Z_g (incl. the current token),
-//           their scores I_j (from TMEM S) and argmin key -> rank 0's `kready`; the ranks split the
+//   exchange (no cluster-wide barrier on the way): each CTA pushes (m_g, Z_g) and the slice of o_g
+//           each rank combines into every rank's inbox with st.async (complete_tx on the receiver's
+//           `xready`); all ranks compute M_g, Z_g (incl. the current token), their scores I_j
+//           (from TMEM S) and argmin key -> st.async into rank 0's `kready`; the ranks split the
 //           output combine; rank 0 picks the slot (lowest index on ties) and evicts in place
-//           (Fig. 2); `xfree` arrivals release the exchange buffers.
+//           (Fig. 2); `xfree` arrivals release the inboxes for the cluster's next unit.
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
