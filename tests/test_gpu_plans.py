@@ -62,6 +62,34 @@ def test_plan_family_lockstep(cuda_lib, S, k, solo, lat):
     assert st.evictions == 2 * B * Hkv and st.max_out_err < 1e-4, (plan, st)
 
 
+# Latency-regime plans (steps below 64 MB) the planner's fitted latency model must pick: the best
+# measured plan of each point in profiles/r02_lat_explore2.jsonl (B, Hq, Hkv, N) -> (S, split_tokens,
+# CTAs per SM, latency variant)
+LATENCY_PICKS = [
+    ((1, 28, 4, 2048), (16, 128, 2, 1)),   # configs[1] (q7)
+    ((2, 32, 8, 512), (4, 128, 2, 1)),     # round 1 kept this on whole units: 10.3 -> 6.6 us
+    ((1, 32, 8, 1024), (8, 128, 2, 1)),
+    ((4, 32, 8, 1024), (4, 256, 2, 1)),
+    ((16, 32, 8, 512), (2, 256, 2, 1)),
+]
+
+
+@pytest.mark.parametrize("shape,pick", LATENCY_PICKS, ids=lambda v: "x".join(map(str, v)))
+def test_latency_regime_auto_plan(cuda_lib, shape, pick):
+    """The automatic plan of small steps is the measured-best family, and it matches the oracle."""
+    from paper_2603_11504_b200 import Cache
+    B, Hq, Hkv, N = shape
+    c = Cache(B, Hq, Hkv, 128, N)
+    plan = c.plan()
+    c.close()
+    got = (plan["splits"], plan["split_tokens"], 2 if plan["tmem_cols"] == 256 else 1, plan["latency_variant"])
+    assert plan["kernel"] == "tcgen05" and got == pick, plan
+    wl = Workload("lat", B, Hq, Hkv, 128, N, N - 1, 3)
+    cache, orc, syn = setup_pair(wl, seed=B * 7 + N, nthreads=8)
+    st = run_lockstep(cache, orc, syn, wl.steps)
+    assert st.evictions == 2 * B * Hkv and st.max_out_err < 1e-4, (plan, st)
+
+
 def _shard_run(wl, P, steps, seed, out_dtype, plan_shards=0, **kw):
     """Steps the whole batch on one cache and, on the same GPU, P shard caches of B/P sequences
     each (plan_batch = B, seq_offset = r B/P; both with the same plan_shards), on the same inputs.
