@@ -918,18 +918,20 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
             }
             ptx::named_bar_sync(1, kNS);                                // red[] and ost complete
             if (sidx == 0) LF_EVENT(ui, 10);
-            if (sidx < S * G) {                                         // (m_g, Z_g) -> rank t
-                const int t = sidx / G, g = sidx % G;
+            // thread -> (rank, element) maps by shifts, not divisions (G <= 8; E4 padded to a power of two)
+            if ((sidx & 7) < G && (sidx >> 3) < S) {                   // (m_g, Z_g) -> rank t
+                const int t = sidx >> 3, g = sidx & 7;
                 const float mm = unit_max(g);
                 const float zz = unit_z(g, g0);
                 ptx::st_async_f32x2(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, mz) + 8 * (s * 16 + g), t), mm, zz,
                                     ptx::mapa(xr_local, t));
             }
-            for (int e = sidx; e < S * E4; e += kNS) {                  // o slice of rank t -> rank t
-                const int t = e / E4, i4 = t * E4 + e % E4;
-                if (i4 < G * 32) {
+            const int lgE = E4 > 1 ? 32 - __clz(E4 - 1) : 0;         // E4 <= 2^lgE
+            for (int e = sidx; e < (S << lgE); e += kNS) {              // o slice of rank t -> rank t
+                const int t = e >> lgE, i = e & ((1 << lgE) - 1), i4 = t * E4 + i;
+                if (i < E4 && i4 < G * 32) {
                     const float4 v4 = *(const float4*)(ost + 4 * i4);
-                    ptx::st_async_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * (s * E4 + e % E4), t), v4,
+                    ptx::st_async_f32x4(ptx::mapa(xc_addr + (uint32_t)offsetof(Xchg, o) + 16 * (s * E4 + i), t), v4,
                                         ptx::mapa(xr_local, t));
                 }
             }
