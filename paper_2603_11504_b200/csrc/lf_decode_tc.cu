@@ -333,6 +333,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
         // ------------------------------ producer -------------------------------------------------
         if constexpr (kLat) {
             uint32_t it = 0, qi = 0;
+            int rst = 0;          // ring stage / phase of load `it`, kept incrementally
+            uint32_t rph = 0;
             for (int i = 0;; ++i, ++qi) {
                 // every global read of the item goes out at once (Q rows, fill state):
                 // one L2 round trip instead of a chain of them before the first MMA
@@ -348,8 +350,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 const int nval = __ldcg(p.n_valid + u);
                 const bool one = x.split && p.chunk == 128;
                 auto issue = [&](int i) {
-                    const int st = it % ST;
-                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                    const int st = rst;
+                    ptx::mbar_wait(BAR(EMPTY + st), rph ^ 1u);
                     ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
                     const int tile = i < x.ntiles ? i : i - x.ntiles;
                     const int row = (p.unit_base + u) * N + x.c0 + tile * 128;
@@ -358,6 +360,10 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     LF_TILE_EVENT(qi, 34, i);
                     ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
                     ++it;
+                    if (++rst == ST) {
+                        rst = 0;
+                        rph ^= 1u;
+                    }
                 };
                 if (one) {   // K and V tile 0 go out before the fill state returns (one round trip less)
                     x.ntiles = 1;
@@ -393,9 +399,13 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
                 }
                 it = __shfl_sync(0xffffffffu, it, 0);
+                rst = __shfl_sync(0xffffffffu, rst, 0);
+                rph = __shfl_sync(0xffffffffu, rph, 0);
             }
         } else {
             uint32_t it = 0, qi = 0;
+            int rst = 0;          // ring stage / phase of load `it`, kept incrementally
+            uint32_t rph = 0;
             for (int i = 0;; ++i, ++qi) {
                 UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
@@ -410,8 +420,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 // the first ring stages go out before Q is staged (they do not depend on it)
                 const int pre = min(2 * x.ntiles, ST);
                 auto issue = [&](int i) {
-                    const int st = it % ST;
-                    ptx::mbar_wait(BAR(EMPTY + st), ((it / ST) & 1u) ^ 1u);
+                    const int st = rst;
+                    ptx::mbar_wait(BAR(EMPTY + st), rph ^ 1u);
                     ptx::mbar_arrive_expect_tx(BAR(FULL + st), kStageBytes);
                     const int tile = i < x.ntiles ? i : i - x.ntiles;
                     const int row = (p.unit_base + u) * N + x.c0 + tile * 128;
@@ -420,6 +430,10 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     LF_TILE_EVENT(qi, 34, i);
                     ptx::tma_load_3d(dst, tm, BAR(FULL + st), 0, row, 0);   // both 64-column halves
                     ++it;
+                    if (++rst == ST) {
+                        rst = 0;
+                        rph ^= 1u;
+                    }
                 };
                 if (lane == 0)
                     for (int i = 0; i < pre; ++i) issue(i);
@@ -439,6 +453,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     for (int i = pre; i < 2 * x.ntiles; ++i) issue(i);
                 }
                 it = __shfl_sync(0xffffffffu, it, 0);
+                rst = __shfl_sync(0xffffffffu, rst, 0);
+                rph = __shfl_sync(0xffffffffu, rph, 0);
             }
         }
     } else if (warp == 1) {
@@ -453,6 +469,8 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
             constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(128, 8, 0, 0);
             constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(128, 16, 1, 0);
             uint32_t it = 0, pi = 0, ui = 0;
+            int rst = 0;          // ring stage of load `it` and its phase, kept incrementally (no
+            uint32_t rph = 0;     // runtime division by ST on the per-tile issue path)
             for (int i = 0;; ++i, ++ui) {
                 UnitInfo x = item_base(p, cid, s, C, i);
                 if (!x.valid) break;
@@ -467,9 +485,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 ptx::tc_fence_after();
                 const uint32_t qbase = qsm + par * 4096;
                 const uint32_t sreg = tmem + par * RC;
-                for (int t = 0; t < x.ntiles; ++t, ++it) {                  // S^T = K_tile . Q^T
-                    const int st = it % ST;
-                    ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                for (int t = 0; t < x.ntiles; ++t, ++it, (++rst == ST ? (rst = 0, rph ^= 1u) : 0u)) {   // S^T = K . Q^T
+                    const int st = rst;
+                    ptx::mbar_wait(BAR(FULL + st), rph);
                     LF_TILE_EVENT(ui, 32, t);
                     ptx::tc_fence_after();
                     const uint32_t base = ring + (uint32_t)st * kStageBytes;
@@ -494,9 +512,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                 }
                 __syncwarp();
                 const uint32_t oreg = tmem + (par ^ 1u) * RC;
-                for (int t = 0; t < x.ntiles; ++t, ++it, ++pi) {          // O^T += V^T . P^T
-                    const int st = it % ST;
-                    ptx::mbar_wait(BAR(FULL + st), (it / ST) & 1u);
+                for (int t = 0; t < x.ntiles; ++t, ++it, ++pi, (++rst == ST ? (rst = 0, rph ^= 1u) : 0u)) {   // O^T += V^T . P^T
+                    const int st = rst;
+                    ptx::mbar_wait(BAR(FULL + st), rph);
                     const int pb = pi % kNPB;
                     ptx::mbar_wait(BAR(PREADY + pb), (pi / kNPB) & 1u);
                     ptx::tc_fence_after();
@@ -736,7 +754,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
             // V tiles go round-robin over the groups across units (c = the CTA's tile count), so the
             // tiles t = s, s + kNG, ... of this unit (subset s) are all handled by group (pi + s) % kNG
             const int g0 = (int)(pi % kNG);   // group of subset 0 in this unit
-            for (int t = 0; t < x.ntiles; ++t) {
+            int vst = (int)((it + x.ntiles) % ST);                     // ring stage / phase of V load t
+            uint32_t vph = ((it + x.ntiles) / ST) & 1u;
+            for (int t = 0; t < x.ntiles; ++t, (++vst == ST ? (vst = 0, vph ^= 1u) : 0u)) {
                 const uint32_t c = pi + t;
                 if ((int)(c % kNG) != grp) continue;
                 const int pb = c % kNPB;   // a single group alternates two P buffers, so it writes
@@ -767,10 +787,9 @@ __global__ void __launch_bounds__(64 + 128 * kNG, kNG == 1 ? 2 : 1) tc_decode_ke
                     *(uint16_t*)(P + (8 + g) * 128 + ((((cc >> 3) ^ g) & 7) << 4) + (cc & 7) * 2) = lo;
                 }
                 if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 26);
-                const uint32_t iv = it + x.ntiles + t;
-                const int st = iv % ST;
+                const int st = vst;
                 if (!lam_first) {
-                ptx::mbar_wait(BAR(FULL + st), (iv / ST) & 1u);      // V tile landed
+                ptx::mbar_wait(BAR(FULL + st), vph);      // V tile landed
                 if (t == 0 && q4 == 0 && lane == 0) LF_EVENT(ui, 5);
                 unsigned char* Vt = smem + so.ring + st * kStageBytes;
                 if (!valid) {   // rows past n may hold stale data: P = 0 must not meet Inf/NaN
